@@ -1,0 +1,136 @@
+/*
+ * dsfft.h -- C ABI of the B200-native batched dual-select FFT (libdsfft.so).
+ *
+ * This is the drop-in boundary for the reference's plan/execute hot path
+ * (arxiv/paper_2604_00567 "fmafft", /root/reference/proj/core).  Plain
+ * pointers and sizes only; no C++ or torch types cross it.  Each entry point
+ * names the reference interface it replaces (file:line under
+ * /root/reference/proj/core/).  The C++ mirror of the reference API lives in
+ * include/fmafft_b200.hpp; INTEGRATION.md shows the bindings.
+ *
+ * Enumerations keep the reference's declaration order so values cast 1:1:
+ *   dsfft_strategy  == fmafft::Strategy     (include/fmafft/twiddle.hpp:14)
+ *   dsfft_precision == fmafft::Precision    (include/fmafft/precision.hpp:12)
+ *
+ * Sample layout on device and in the *_host working-precision calls:
+ * interleaved complex in the working precision, transform-major:
+ *   fp16: binary16 pairs (re, im) = 4 bytes per sample
+ *   fp32: binary32 pairs (re, im) = 8 bytes per sample
+ * Buffers must be 16-byte aligned.  in == out (in place) is allowed.
+ *
+ * Errors: every int-returning call returns a dsfft_status; on failure
+ * dsfft_last_error() holds the reference's exception text where one exists
+ * (e.g. "FFT size must be a power of two >= 2, got 1023").  NaN/inf data is
+ * never an error: it propagates exactly as in the reference.
+ */
+#ifndef DSFFT_H
+#define DSFFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSFFT_VERSION 1
+
+typedef enum {
+  DSFFT_STANDARD = 0,
+  DSFFT_LINZER_FEIG = 1,
+  DSFFT_COSINE = 2,
+  DSFFT_DUAL_SELECT = 3
+} dsfft_strategy;
+
+typedef enum { DSFFT_FP16 = 0, DSFFT_FP32 = 1, DSFFT_FP64 = 2 } dsfft_precision;
+
+typedef enum { DSFFT_FORWARD = 0, DSFFT_INVERSE = 1 } dsfft_direction;
+
+typedef enum {
+  DSFFT_OK = 0,
+  DSFFT_ERR_INVALID = 1,     /* reference: std::invalid_argument */
+  DSFFT_ERR_UNSUPPORTED = 2, /* valid for the reference, not on this device path */
+  DSFFT_ERR_CUDA = 3,        /* CUDA runtime / launch failure */
+  DSFFT_ERR_NO_DEVICE = 4    /* no sm_100 device: the product never falls back to CPU */
+} dsfft_status;
+
+typedef struct dsfft_plan_s* dsfft_plan;
+
+/* One rounded table record == fmafft::TwiddleEntry (twiddle.hpp:26-41). */
+typedef struct {
+  double multiplier;
+  double ratio;
+  int32_t path; /* 0 COS, 1 SIN */
+  int32_t clamped;
+  double omega_r;
+  double omega_i;
+} dsfft_entry;
+
+/* Replaces fmafft::make_plan(n, strategy, precision)        (fft.hpp:26, fft.cpp:56-72)
+ * and build_table(n, s, clamp_eps)                          (twiddle.hpp:65).
+ * Builds the FP64 table on the host with the reference algorithm (libm
+ * cos/sin, Algorithm 1 with the >= tie to COS), rounds it once into the working
+ * precision, packs the per-stage device records and uploads them to `device`.
+ * n: power of two in [2, 2^24]; clamp_eps > 0 (used by linzer_feig only). */
+int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, int device,
+                      dsfft_plan* out);
+
+int dsfft_plan_destroy(dsfft_plan plan);
+
+/* FftPlan fields (fft.hpp:17-23). */
+int dsfft_plan_info(dsfft_plan plan, size_t* n, unsigned* m, int* strategy, int* precision);
+
+/* Host-only table builder (no device needed): make_plan's table, i.e.
+ * build_table(n, strategy, clamp_eps) (twiddle.cpp:133-141) rounded once into
+ * `precision` (fft.cpp:65-70); precision fp64 returns the raw FP64 table.
+ * `out` receives n/2 records. */
+int dsfft_build_table(size_t n, int strategy, int precision, double clamp_eps, dsfft_entry* out,
+                      size_t count);
+
+/* Copy of the plan's rounded table: FftPlan::table.entries (n/2 records). */
+int dsfft_plan_table(dsfft_plan plan, dsfft_entry* out, size_t count);
+
+/* Batched forward / inverse on device buffers, enqueued on `stream`
+ * (cudaStream_t; NULL = legacy default stream).  Replaces
+ *   SampleBuffer forward(const FftPlan&, const SampleBuffer&, ArithmeticContext&)  (fft.hpp:33-34)
+ *   SampleBuffer inverse(const FftPlan&, const SampleBuffer&, ArithmeticContext&)  (fft.hpp:38-39)
+ * for `batch` independent transforms.  Input must already be in the working
+ * precision (the reference's ingest rounding, fft.cpp:79-82, is dsfft_round_to).
+ * Bit-identical to the reference in fp32 and fp16. */
+int dsfft_execute(dsfft_plan plan, int direction, const void* d_in, void* d_out, size_t batch,
+                  void* stream);
+
+/* Same, from and to HOST buffers in the working precision (pinned memory
+ * gives full PCIe overlap).  Copies are chunked and pipelined against the
+ * kernels on internal streams ordered after / before `stream`; returns after
+ * the results are in h_out. */
+int dsfft_execute_host(dsfft_plan plan, int direction, const void* h_in, void* h_out,
+                       size_t batch, void* stream);
+
+/* The reference's exact calling convention: double-carrier SampleBuffers
+ * (interleaved re, im doubles, fft.hpp:12).  Rounds on ingest with round_to
+ * semantics, runs on the device, widens the result back to double. */
+int dsfft_execute_f64(dsfft_plan plan, int direction, const double* in, double* out,
+                      size_t batch);
+
+/* round_to (precision.cpp:61-75) of `count` doubles into the working format
+ * (binary16 / binary32 words), and the exact widening back. */
+int dsfft_round_to(const double* in, void* out, size_t count, int precision);
+int dsfft_widen(const void* in, double* out, size_t count, int precision);
+
+/* Bytes of one complex sample in the working precision (4, 8), 0 if invalid. */
+size_t dsfft_sample_bytes(int precision);
+
+/* Number of device kernel launches the last execute on this thread issued. */
+uint64_t dsfft_last_launch_count(void);
+
+/* Thread-local text of the last failure ("" when none). */
+const char* dsfft_last_error(void);
+
+int dsfft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSFFT_H */

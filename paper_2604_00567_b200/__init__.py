@@ -1,0 +1,267 @@
+"""B200-native batched dual-select FFT (arXiv 2604.00567) -- Python host side.
+
+A thin mirror of the reference's plan/execute API (``fmafft::make_plan``,
+``forward``, ``inverse``, ``Strategy``, ``Precision``; /root/reference/proj/core/
+include/fmafft/{fft,twiddle,precision}.hpp) over the C ABI of ``libdsfft.so``
+(include/dsfft.h).  All compute runs in the sm_100a kernels; if the library is
+missing or no B200 is present, calls raise -- there is no CPU fallback.
+
+Device API (torch tensors are used as plain device buffers):
+    plan = make_plan(1024, "dual", "fp16")
+    y = forward(plan, x)      # x: cuda tensor [batch, n] complex32/complex64
+                              #    or [batch, n, 2] float16/float32
+Reference calling convention (double-carrier SampleBuffers, ingest rounding):
+    y = forward_f64(plan, x)  # x: numpy complex128 [batch, n] or [n]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["Strategy", "Precision", "FftPlan", "make_plan", "forward", "inverse",
+           "execute", "forward_f64", "inverse_f64", "execute_host", "round_to", "widen",
+           "parse_strategy", "parse_precision", "library_path", "DsfftError"]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libdsfft.so")
+
+# fmafft::Strategy / Precision declaration order (twiddle.hpp:14, precision.hpp:12)
+STRATEGIES = {"standard": 0, "lf": 1, "cosine": 2, "dual": 3}
+PRECISIONS = {"fp16": 0, "fp32": 1, "fp64": 2}
+_STRATEGY_ALIASES = {"standard": "standard", "lf": "lf", "linzer-feig": "lf",
+                     "linzer_feig": "lf", "cosine": "cosine", "dual": "dual",
+                     "dual-select": "dual", "dual_select": "dual"}
+
+
+class Strategy:
+    standard = "standard"
+    linzer_feig = "lf"
+    cosine = "cosine"
+    dual_select = "dual"
+
+
+class Precision:
+    fp16 = "fp16"
+    fp32 = "fp32"
+    fp64 = "fp64"
+
+
+def parse_strategy(name: str) -> str:
+    """twiddle.cpp:45-53 (throws std::invalid_argument -> ValueError)."""
+    try:
+        return _STRATEGY_ALIASES[name]
+    except KeyError:
+        raise ValueError(f"unknown strategy: {name}") from None
+
+
+def parse_precision(name: str) -> str:
+    """precision.cpp:54-59."""
+    if name not in PRECISIONS:
+        raise ValueError(f"unknown precision: {name}")
+    return name
+
+
+class DsfftError(RuntimeError):
+    pass
+
+
+class _Entry(C.Structure):
+    _fields_ = [("multiplier", C.c_double), ("ratio", C.c_double), ("path", C.c_int32),
+                ("clamped", C.c_int32), ("omega_r", C.c_double), ("omega_i", C.c_double)]
+
+
+ENTRY_DTYPE = np.dtype([("multiplier", "<f8"), ("ratio", "<f8"), ("path", "<i4"),
+                        ("clamped", "<i4"), ("omega_r", "<f8"), ("omega_i", "<f8")])
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is not built; run `python -m paper_2604_00567_b200.build`"
+                          " (there is no CPU fallback)")
+    lib = C.CDLL(_LIB_PATH)
+    vp, sz, i = C.c_void_p, C.c_size_t, C.c_int
+    lib.dsfft_last_error.restype = C.c_char_p
+    lib.dsfft_plan_create.argtypes = [sz, i, i, C.c_double, i, C.POINTER(vp)]
+    lib.dsfft_plan_destroy.argtypes = [vp]
+    lib.dsfft_plan_info.argtypes = [vp, C.POINTER(sz), C.POINTER(C.c_uint), C.POINTER(i),
+                                    C.POINTER(i)]
+    lib.dsfft_plan_table.argtypes = [vp, vp, sz]
+    lib.dsfft_build_table.argtypes = [sz, i, i, C.c_double, vp, sz]
+    lib.dsfft_execute.argtypes = [vp, i, vp, vp, sz, vp]
+    lib.dsfft_execute_host.argtypes = [vp, i, vp, vp, sz, vp]
+    lib.dsfft_execute_f64.argtypes = [vp, i, vp, vp, sz]
+    lib.dsfft_round_to.argtypes = [vp, vp, sz, i]
+    lib.dsfft_widen.argtypes = [vp, vp, sz, i]
+    lib.dsfft_sample_bytes.restype = sz
+    lib.dsfft_sample_bytes.argtypes = [i]
+    lib.dsfft_last_launch_count.restype = C.c_uint64
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = _load().dsfft_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)            # std::invalid_argument in the reference
+    if rc == 2:
+        raise NotImplementedError(msg)
+    raise DsfftError(msg)
+
+
+@dataclass
+class FftPlan:
+    """Mirror of fmafft::FftPlan (fft.hpp:17-23) owning a device plan."""
+    n: int
+    m: int
+    strategy: str
+    precision: str
+    device: int
+    _handle: C.c_void_p
+
+    @property
+    def table(self) -> np.ndarray:
+        """FftPlan::table.entries: the rounded n/2 records (TwiddleEntry fields)."""
+        out = np.zeros(max(self.n // 2, 1), dtype=ENTRY_DTYPE)
+        _check(_load().dsfft_plan_table(self._handle, out.ctypes.data, out.size))
+        return out[: self.n // 2]
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h and _lib is not None:
+            _lib.dsfft_plan_destroy(h)
+            self._handle = None
+
+
+def make_plan(n: int, strategy: str = "dual", precision: str = "fp32",
+              clamp_eps: float = 1e-7, device: int = 0) -> FftPlan:
+    """fmafft::make_plan (fft.cpp:56-72): n a power of two in [2, 2^24]."""
+    strategy = parse_strategy(strategy)
+    precision = parse_precision(precision)
+    h = C.c_void_p()
+    _check(_load().dsfft_plan_create(int(n), STRATEGIES[strategy], PRECISIONS[precision],
+                                     float(clamp_eps), int(device), C.byref(h)))
+    m = int(n).bit_length() - 1
+    return FftPlan(int(n), m, strategy, precision, device, h)
+
+
+def build_table(n: int, strategy: str, precision: str = "fp64",
+                clamp_eps: float = 1e-7) -> np.ndarray:
+    """Host table builder: make_plan's rounded table (fp64: build_table)."""
+    out = np.zeros(max(int(n) // 2, 1), dtype=ENTRY_DTYPE)
+    _check(_load().dsfft_build_table(int(n), STRATEGIES[parse_strategy(strategy)],
+                                     PRECISIONS[parse_precision(precision)], float(clamp_eps),
+                                     out.ctypes.data, out.size))
+    return out[: int(n) // 2]
+
+
+def sample_bytes(precision: str) -> int:
+    return 4 if precision == "fp16" else 8 if precision == "fp32" else 16
+
+
+def _torch_view(x, plan: FftPlan):
+    import torch
+    want_c = torch.complex32 if plan.precision == "fp16" else torch.complex64
+    want_r = torch.float16 if plan.precision == "fp16" else torch.float32
+    if x.dtype == want_c:
+        n = x.shape[-1]
+    elif x.dtype == want_r and x.shape[-1] == 2:
+        n = x.shape[-2]
+    else:
+        raise ValueError(f"{plan.precision} plan needs {want_c} or {want_r}[..., 2] data, "
+                         f"got {x.dtype}")
+    if n != plan.n:
+        raise ValueError(f"buffer length {n} does not match plan size {plan.n}")
+    if not x.is_cuda:
+        raise ValueError("device API needs a CUDA tensor (use forward_f64 for host data)")
+    if not x.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    batch = x.numel() // (plan.n * (2 if x.dtype == want_r else 1))
+    return batch
+
+
+def execute(plan: FftPlan, direction: int, x, out=None, stream=None):
+    """Batched transform of a CUDA tensor (direction 0 forward, 1 inverse)."""
+    import torch
+    batch = _torch_view(x, plan)
+    if out is None:
+        out = torch.empty_like(x)
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    _check(_load().dsfft_execute(plan._handle, direction, x.data_ptr(), out.data_ptr(), batch,
+                                 stream))
+    return out
+
+
+def forward(plan: FftPlan, x, out=None, stream=None):
+    """fmafft::forward (fft.hpp:33) on a batch of device transforms."""
+    return execute(plan, 0, x, out, stream)
+
+
+def inverse(plan: FftPlan, x, out=None, stream=None):
+    """fmafft::inverse (fft.hpp:38) on a batch of device transforms."""
+    return execute(plan, 1, x, out, stream)
+
+
+def execute_host(plan: FftPlan, direction: int, h_in: np.ndarray, h_out: np.ndarray,
+                 batch: int, stream: int = 0) -> None:
+    """Host buffers in the working precision (pinned for full overlap)."""
+    _check(_load().dsfft_execute_host(plan._handle, direction, h_in.ctypes.data,
+                                      h_out.ctypes.data, batch, stream))
+
+
+def _f64_call(plan: FftPlan, direction: int, x) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    if x.shape[-1] != plan.n:
+        raise ValueError(f"buffer length {x.shape[-1]} does not match plan size {plan.n}")
+    out = np.empty_like(x)
+    batch = x.size // plan.n
+    _check(_load().dsfft_execute_f64(plan._handle, direction, x.ctypes.data, out.ctypes.data,
+                                     batch))
+    return out
+
+
+def forward_f64(plan: FftPlan, x) -> np.ndarray:
+    """The reference's exact convention: complex128 in, ingest round_to, device
+    transform, result widened to complex128 (SampleBuffer, fft.hpp:12)."""
+    return _f64_call(plan, 0, x)
+
+
+def inverse_f64(plan: FftPlan, x) -> np.ndarray:
+    return _f64_call(plan, 1, x)
+
+
+def round_to(x, precision: str) -> np.ndarray:
+    """round_to (precision.cpp:61-75) through the product's own converter."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    p = PRECISIONS[parse_precision(precision)]
+    dt = {0: np.uint16, 1: np.float32, 2: np.float64}[p]
+    raw = np.empty(x.shape, dtype=dt)
+    _check(_load().dsfft_round_to(x.ctypes.data, raw.ctypes.data, x.size, p))
+    return raw
+
+
+def widen(raw: np.ndarray, precision: str) -> np.ndarray:
+    p = PRECISIONS[parse_precision(precision)]
+    raw = np.ascontiguousarray(raw)
+    out = np.empty(raw.shape, dtype=np.float64)
+    _check(_load().dsfft_widen(raw.ctypes.data, out.ctypes.data, raw.size, p))
+    return out
+
+
+def last_launch_count() -> int:
+    return int(_load().dsfft_last_launch_count())

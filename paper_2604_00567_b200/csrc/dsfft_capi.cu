@@ -1,0 +1,481 @@
+// dsfft_capi.cu -- C ABI (include/dsfft.h): plans, device upload, dispatch,
+// host-buffer pipelines.  The only compute path is the sm_100a kernels; there
+// is no CPU fallback: without an sm_100 device every execute fails loudly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dsfft.h"
+#include "host_table.hpp"
+#include "multipass.cuh"
+#include "small_launch.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(DSFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define DSFFT_CUDA(call)                                 \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+const dsfft::SmallEntry& small_entry(int m) {
+  static const dsfft::SmallEntry table[13] = {
+      {},
+      dsfft::small_entry_m1(),  dsfft::small_entry_m2(),  dsfft::small_entry_m3(),
+      dsfft::small_entry_m4(),  dsfft::small_entry_m5(),  dsfft::small_entry_m6(),
+      dsfft::small_entry_m7(),  dsfft::small_entry_m8(),  dsfft::small_entry_m9(),
+      dsfft::small_entry_m10(), dsfft::small_entry_m11(), dsfft::small_entry_m12()};
+  return table[m];
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Host-buffer pipeline: NSLOT chunk slots, each with its own stream and
+// device in/out buffers, so H2D(i+1) / kernel(i) / D2H(i-1) overlap.
+struct HostPipe {
+  static constexpr int kSlots = 3;
+  size_t chunk_bytes = 0;
+  void* d_in[kSlots] = {};
+  void* d_out[kSlots] = {};
+  cudaStream_t st[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  cudaEvent_t start = nullptr;
+  ~HostPipe() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (d_in[i]) cudaFree(d_in[i]);
+      if (d_out[i]) cudaFree(d_out[i]);
+      if (st[i]) cudaStreamDestroy(st[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+    if (start) cudaEventDestroy(start);
+  }
+};
+
+}  // namespace
+
+struct dsfft_plan_s {
+  size_t n = 0;
+  unsigned m = 0;
+  int strategy = 0, precision = 0, device = 0;
+  double clamp_eps = 1e-7;
+  std::vector<dsfft::TableEntry> table;  // rounded (FftPlan::table)
+  // single-kernel path (m <= 12)
+  const dsfft::SmallEntry* small = nullptr;
+  uint4* d_tw = nullptr;
+  int groups = 0, stages = 0, grid = 0;
+  // multi-pass path (m > 12)
+  dsfft::MultipassPlan* mp = nullptr;
+  int sm_count = 0;
+  size_t smem_optin = 0;
+  std::mutex mu;
+  HostPipe* pipe = nullptr;
+  uint8_t* scratch = nullptr;  // 16-byte-aligned tail staging (N=2 fp16, odd batch)
+};
+
+namespace {
+
+size_t sample_bytes(int p) { return p == DSFFT_FP16 ? 4 : p == DSFFT_FP32 ? 8 : 0; }
+
+uint32_t inverse_scale_word(const dsfft_plan_s* p) {
+  const double s = dsfft::round_to(1.0 / double(p->n), p->precision);  // fft.cpp:92-93
+  if (p->precision == DSFFT_FP16) {
+    const uint32_t h = dsfft::half_bits(s);
+    return h | (h << 16);
+  }
+  const float f = float(s);
+  uint32_t b;
+  std::memcpy(&b, &f, 4);
+  return b;
+}
+
+// Choose groups per CTA and buffers per group for the single-kernel path.
+void choose_small_launch(dsfft_plan_s* p) {
+  const dsfft::SmallGeom& g = p->small->geom;
+  const int T = 32 * g.warps;
+  int stages = env_int("DSFFT_STAGES", 3);
+  stages = std::max(2, std::min(stages, 8));
+  int max_groups = std::max(1, g.max_threads / T);
+  int want = env_int("DSFFT_GROUPS", 0);
+  int groups = 0;
+  for (int ng = max_groups; ng >= 1; --ng) {
+    if (p->small->smem_bytes(ng, stages) <= p->smem_optin) {
+      groups = ng;
+      break;
+    }
+  }
+  while (groups == 0 && stages > 2) {  // shrink the ring if even one group does not fit
+    --stages;
+    if (p->small->smem_bytes(1, stages) <= p->smem_optin) groups = 1;
+  }
+  if (want > 0 && want <= max_groups && p->small->smem_bytes(want, stages) <= p->smem_optin)
+    groups = want;
+  p->groups = std::max(1, groups);
+  p->stages = stages;
+  p->grid = p->sm_count * std::max(1, env_int("DSFFT_CTAS_PER_SM", 1));
+}
+
+int upload_small_tables(dsfft_plan_s* p) {
+  const dsfft::SmallGeom& g = p->small->geom;
+  std::vector<dsfft::Record> rec(g.tw_records);
+  for (int st = 0; st < g.nstage; ++st) {
+    const int P = g.P[st], s = g.s[st];
+    for (int pl = 0; pl < s; ++pl)
+      for (int rl = 0; rl < (1 << pl); ++rl)
+        for (int r = 0; r < (1 << P); ++r) {
+          const int slot = g.tw_off[st] + dsfft::tw_slot(P, r, pl, rl);
+          const int k = dsfft::tw_entry(int(p->m), P, r, pl, rl);
+          rec[slot] = dsfft::pack_record(p->table[k], p->strategy, p->precision);
+        }
+  }
+  DSFFT_CUDA(cudaMalloc(&p->d_tw, rec.size() * sizeof(dsfft::Record)));
+  DSFFT_CUDA(cudaMemcpy(p->d_tw, rec.data(), rec.size() * sizeof(dsfft::Record),
+                        cudaMemcpyHostToDevice));
+  return DSFFT_OK;
+}
+
+// Launch the batched transform on device buffers (no argument checks).
+int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
+           cudaStream_t stream) {
+  if (batch == 0) return DSFFT_OK;
+  const bool f16 = p->precision == DSFFT_FP16;
+  const uint32_t scale = inverse_scale_word(p);
+  if (p->mp) {
+    const int e = dsfft::multipass_execute(*p->mp, dir == DSFFT_INVERSE, in, out, batch, scale,
+                                           stream, &g_launches);
+    if (e) return fail(DSFFT_ERR_CUDA, dsfft::multipass_error());
+    return DSFFT_OK;
+  }
+  const dsfft::SmallGeom& g = p->small->geom;
+  const size_t tb = p->n * sample_bytes(p->precision);
+  const long long tpi = (f16 ? 2LL : 1LL) * g.k;
+  // bulk copies move multiples of 16 bytes: N=2 fp16 with an odd batch
+  // stages its last transform through a padded scratch buffer
+  size_t main_batch = batch;
+  if ((batch * tb) % 16 != 0) main_batch = batch - 1;
+  if (main_batch) {
+    dsfft::LaunchArgs a{};
+    a.f16 = f16;
+    a.standard = p->strategy == DSFFT_STANDARD;
+    a.inverse = dir == DSFFT_INVERSE;
+    a.kp.in = static_cast<const uint8_t*>(in);
+    a.kp.out = static_cast<uint8_t*>(out);
+    a.kp.tw = p->d_tw;
+    a.kp.batch = (long long)main_batch;
+    a.kp.n_items = ((long long)main_batch + tpi - 1) / tpi;
+    a.kp.scale = scale;
+    a.kp.stages = p->stages;
+    a.stream = stream;
+    a.groups = p->groups;
+    a.grid = int(std::min<long long>(p->grid, (a.kp.n_items + p->groups - 1) / p->groups));
+    cudaError_t e = p->small->launch(a);
+    if (e != cudaSuccess) return cuda_fail(e, "fft_small_kernel launch");
+    ++g_launches;
+  }
+  if (main_batch != batch) {
+    if (!p->scratch) DSFFT_CUDA(cudaMalloc(&p->scratch, 64));
+    const size_t off = main_batch * tb;
+    DSFFT_CUDA(cudaMemcpyAsync(p->scratch, static_cast<const uint8_t*>(in) + off, tb,
+                               cudaMemcpyDeviceToDevice, stream));
+    dsfft::LaunchArgs a{};
+    a.f16 = f16;
+    a.standard = p->strategy == DSFFT_STANDARD;
+    a.inverse = dir == DSFFT_INVERSE;
+    a.kp.in = p->scratch;
+    a.kp.out = p->scratch;
+    a.kp.tw = p->d_tw;
+    a.kp.batch = 2;  // pad to a 16-byte transfer; the second transform is discarded
+    a.kp.n_items = 1;
+    a.kp.scale = scale;
+    a.kp.stages = p->stages;
+    a.stream = stream;
+    a.groups = 1;
+    a.grid = 1;
+    cudaError_t e = p->small->launch(a);
+    if (e != cudaSuccess) return cuda_fail(e, "fft_small_kernel launch (tail)");
+    ++g_launches;
+    DSFFT_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(out) + off, p->scratch, tb,
+                               cudaMemcpyDeviceToDevice, stream));
+  }
+  return DSFFT_OK;
+}
+
+int check_exec_args(dsfft_plan_s* p, int dir, const void* in, void* out) {
+  if (!p) return fail(DSFFT_ERR_INVALID, "null plan");
+  if (dir != DSFFT_FORWARD && dir != DSFFT_INVERSE)
+    return fail(DSFFT_ERR_INVALID, "unknown direction");
+  if (p->precision == DSFFT_FP64)
+    return fail(DSFFT_ERR_UNSUPPORTED, "fp64 execution is not on the device path");
+  if (!in || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
+  return DSFFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsfft_last_error(void) { return g_err.c_str(); }
+
+int dsfft_version(void) { return DSFFT_VERSION; }
+
+uint64_t dsfft_last_launch_count(void) { return g_launches; }
+
+size_t dsfft_sample_bytes(int precision) { return sample_bytes(precision); }
+
+int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, int device,
+                      dsfft_plan* out) {
+  g_err.clear();
+  if (!out) return fail(DSFFT_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (precision < DSFFT_FP16 || precision > DSFFT_FP64)
+    return fail(DSFFT_ERR_INVALID, "unknown precision: " + std::to_string(precision));
+  if (strategy < DSFFT_STANDARD || strategy > DSFFT_DUAL_SELECT)
+    return fail(DSFFT_ERR_INVALID, "unknown strategy: " + std::to_string(strategy));
+  auto* p = new dsfft_plan_s();
+  try {
+    p->table = dsfft::plan_table(n, strategy, precision, clamp_eps);
+  } catch (const std::exception& e) {
+    delete p;
+    return fail(DSFFT_ERR_INVALID, e.what());
+  }
+  p->n = n;
+  while ((size_t(1) << p->m) < n) ++p->m;
+  p->strategy = strategy;
+  p->precision = precision;
+  p->clamp_eps = clamp_eps;
+  p->device = device;
+  if (precision == DSFFT_FP64) {  // table-only plan (introspection); execute refuses
+    *out = p;
+    return DSFFT_OK;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete p;
+    cudaGetLastError();
+    return fail(DSFFT_ERR_NO_DEVICE, "no CUDA device: dsfft has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) {
+    delete p;
+    return fail(DSFFT_ERR_INVALID, "device ordinal out of range");
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) {
+    delete p;
+    return fail(DSFFT_ERR_NO_DEVICE, "device is not sm_100 (B200): dsfft is sm_100a-only");
+  }
+  p->sm_count = prop.multiProcessorCount;
+  p->smem_optin = prop.sharedMemPerBlockOptin;
+  DeviceGuard guard(device);
+  int rc = DSFFT_OK;
+  if (p->m <= 12) {
+    p->small = &small_entry(int(p->m));
+    choose_small_launch(p);
+    rc = upload_small_tables(p);
+  } else {
+    p->mp = dsfft::multipass_create(p->table, int(p->m), strategy, precision, p->sm_count,
+                                    p->smem_optin);
+    if (!p->mp) rc = fail(DSFFT_ERR_CUDA, dsfft::multipass_error());
+  }
+  if (rc != DSFFT_OK) {
+    dsfft_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return DSFFT_OK;
+}
+
+int dsfft_plan_destroy(dsfft_plan p) {
+  if (!p) return DSFFT_OK;
+  {
+    DeviceGuard guard(p->device);
+    if (p->d_tw) cudaFree(p->d_tw);
+    if (p->scratch) cudaFree(p->scratch);
+    delete p->pipe;
+    if (p->mp) dsfft::multipass_destroy(p->mp);
+  }
+  delete p;
+  return DSFFT_OK;
+}
+
+int dsfft_plan_info(dsfft_plan p, size_t* n, unsigned* m, int* strategy, int* precision) {
+  if (!p) return fail(DSFFT_ERR_INVALID, "null plan");
+  if (n) *n = p->n;
+  if (m) *m = p->m;
+  if (strategy) *strategy = p->strategy;
+  if (precision) *precision = p->precision;
+  return DSFFT_OK;
+}
+
+int dsfft_build_table(size_t n, int strategy, int precision, double clamp_eps, dsfft_entry* out,
+                      size_t count) {
+  if (!out) return fail(DSFFT_ERR_INVALID, "null argument");
+  std::vector<dsfft::TableEntry> t;
+  try {
+    t = dsfft::plan_table(n, strategy, precision, clamp_eps);
+  } catch (const std::exception& e) {
+    return fail(DSFFT_ERR_INVALID, e.what());
+  }
+  if (count < t.size()) return fail(DSFFT_ERR_INVALID, "output too small");
+  for (size_t k = 0; k < t.size(); ++k) {
+    const auto& e = t[k];
+    out[k] = dsfft_entry{e.multiplier, e.ratio, e.path, e.clamped ? 1 : 0, e.omega_r, e.omega_i};
+  }
+  return DSFFT_OK;
+}
+
+int dsfft_plan_table(dsfft_plan p, dsfft_entry* out, size_t count) {
+  if (!p || !out) return fail(DSFFT_ERR_INVALID, "null argument");
+  if (count < p->table.size()) return fail(DSFFT_ERR_INVALID, "output too small");
+  for (size_t k = 0; k < p->table.size(); ++k) {
+    const auto& e = p->table[k];
+    out[k] = dsfft_entry{e.multiplier, e.ratio, e.path, e.clamped ? 1 : 0, e.omega_r, e.omega_i};
+  }
+  return DSFFT_OK;
+}
+
+int dsfft_execute(dsfft_plan p, int dir, const void* in, void* out, size_t batch, void* stream) {
+  g_launches = 0;
+  int rc = check_exec_args(p, dir, in, out);
+  if (rc) return rc;
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(DSFFT_ERR_INVALID, "device buffers must be 16-byte aligned");
+  DeviceGuard guard(p->device);
+  return launch(p, dir, in, out, batch, static_cast<cudaStream_t>(stream));
+}
+
+int dsfft_execute_host(dsfft_plan p, int dir, const void* h_in, void* h_out, size_t batch,
+                       void* stream_) {
+  g_launches = 0;
+  int rc = check_exec_args(p, dir, h_in, h_out);
+  if (rc) return rc;
+  if (batch == 0) return DSFFT_OK;
+  DeviceGuard guard(p->device);
+  std::lock_guard<std::mutex> lock(p->mu);
+  cudaStream_t user = static_cast<cudaStream_t>(stream_);
+  const size_t tb = p->n * sample_bytes(p->precision);
+  const size_t want_chunk = size_t(env_int("DSFFT_HOST_CHUNK_MB", 32)) << 20;
+  size_t per = std::max<size_t>(1, want_chunk / tb);
+  if (per % 2) per += (per > 1) ? -1 : 1;  // keep fp16 pairs whole
+  const size_t chunk_bytes = per * tb;
+  if (!p->pipe || p->pipe->chunk_bytes < chunk_bytes) {
+    delete p->pipe;
+    p->pipe = new HostPipe();
+    p->pipe->chunk_bytes = chunk_bytes;
+    for (int i = 0; i < HostPipe::kSlots; ++i) {
+      DSFFT_CUDA(cudaMalloc(&p->pipe->d_in[i], chunk_bytes));
+      DSFFT_CUDA(cudaMalloc(&p->pipe->d_out[i], chunk_bytes));
+      DSFFT_CUDA(cudaStreamCreateWithFlags(&p->pipe->st[i], cudaStreamNonBlocking));
+      DSFFT_CUDA(cudaEventCreateWithFlags(&p->pipe->ev[i], cudaEventDisableTiming));
+    }
+    DSFFT_CUDA(cudaEventCreateWithFlags(&p->pipe->start, cudaEventDisableTiming));
+  }
+  HostPipe& hp = *p->pipe;
+  DSFFT_CUDA(cudaEventRecord(hp.start, user));
+  for (int i = 0; i < HostPipe::kSlots; ++i) DSFFT_CUDA(cudaStreamWaitEvent(hp.st[i], hp.start, 0));
+  uint64_t launches = 0;
+  const uint8_t* src = static_cast<const uint8_t*>(h_in);
+  uint8_t* dst = static_cast<uint8_t*>(h_out);
+  size_t done = 0;
+  for (size_t c = 0; done < batch; ++c) {
+    const int slot = int(c % HostPipe::kSlots);
+    const size_t nb = std::min(per, batch - done);
+    cudaStream_t s = hp.st[slot];
+    DSFFT_CUDA(cudaMemcpyAsync(hp.d_in[slot], src + done * tb, nb * tb, cudaMemcpyHostToDevice, s));
+    rc = launch(p, dir, hp.d_in[slot], hp.d_out[slot], nb, s);
+    if (rc) return rc;
+    launches += g_launches;
+    g_launches = 0;
+    DSFFT_CUDA(cudaMemcpyAsync(dst + done * tb, hp.d_out[slot], nb * tb, cudaMemcpyDeviceToHost, s));
+    done += nb;
+  }
+  for (int i = 0; i < HostPipe::kSlots; ++i) {
+    DSFFT_CUDA(cudaEventRecord(hp.ev[i], hp.st[i]));
+    DSFFT_CUDA(cudaStreamWaitEvent(user, hp.ev[i], 0));
+  }
+  DSFFT_CUDA(cudaStreamSynchronize(user));
+  g_launches = launches;
+  return DSFFT_OK;
+}
+
+int dsfft_round_to(const double* in, void* out, size_t count, int precision) {
+  if (!in || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
+  if (precision == DSFFT_FP16) {
+    auto* o = static_cast<uint16_t*>(out);
+    for (size_t i = 0; i < count; ++i) o[i] = dsfft::half_bits(in[i]);
+  } else if (precision == DSFFT_FP32) {
+    auto* o = static_cast<float*>(out);
+    for (size_t i = 0; i < count; ++i) o[i] = float(dsfft::round_to(in[i], dsfft::kFp32));
+  } else if (precision == DSFFT_FP64) {
+    std::memcpy(out, in, count * sizeof(double));
+  } else {
+    return fail(DSFFT_ERR_INVALID, "unknown precision: " + std::to_string(precision));
+  }
+  return DSFFT_OK;
+}
+
+int dsfft_widen(const void* in, double* out, size_t count, int precision) {
+  if (!in || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
+  if (precision == DSFFT_FP16) {
+    auto* s = static_cast<const uint16_t*>(in);
+    for (size_t i = 0; i < count; ++i) out[i] = dsfft::half_value(s[i]);
+  } else if (precision == DSFFT_FP32) {
+    auto* s = static_cast<const float*>(in);
+    for (size_t i = 0; i < count; ++i) out[i] = double(s[i]);
+  } else if (precision == DSFFT_FP64) {
+    std::memcpy(out, in, count * sizeof(double));
+  } else {
+    return fail(DSFFT_ERR_INVALID, "unknown precision: " + std::to_string(precision));
+  }
+  return DSFFT_OK;
+}
+
+int dsfft_execute_f64(dsfft_plan p, int dir, const double* in, double* out, size_t batch) {
+  g_launches = 0;
+  int rc = check_exec_args(p, dir, in, out);
+  if (rc) return rc;
+  const size_t count = 2 * p->n * batch;
+  std::vector<uint8_t> a(count * (p->precision == DSFFT_FP16 ? 2 : 4) + 16);
+  std::vector<uint8_t> b(a.size());
+  // 16-byte alignment is not needed on the host side (copies are staged)
+  rc = dsfft_round_to(in, a.data(), count, p->precision);
+  if (rc) return rc;
+  rc = dsfft_execute_host(p, dir, a.data(), b.data(), batch, nullptr);
+  if (rc) return rc;
+  return dsfft_widen(b.data(), out, count, p->precision);
+}
+
+}  // extern "C"

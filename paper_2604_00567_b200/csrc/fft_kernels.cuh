@@ -1,0 +1,317 @@
+// fft_kernels.cuh -- the batched single-kernel radix-2 Stockham FFT for sm_100a.
+//
+// One persistent CTA per SM runs NG independent thread groups; each group owns
+// an S-deep ring of item buffers in shared memory.  Per item (K transforms,
+// 8 KiB at N=1024 FP16):
+//   TMA bulk load (cp.async.bulk, mbarrier complete_tx)  -> smem
+//   stage 0: gather 2^s0 values per group into registers, s0 passes in regs
+//   exchange through padded smem (conflict-free, schedule_check.cpp)
+//   stage 1..: same, the last log2(E) passes entirely in registers
+//   natural-order result -> smem -> TMA bulk store (bulk_group)
+// Loads for the next S-1 items are in flight while an item is computed.
+//
+// Arithmetic (the parity contract):
+//  * FMA strategies (LF, cosine, dual) use the branch-free unified form of
+//    cosine_core/sine_core (butterfly.cpp:10-33): the host packs per twiddle
+//    (t, w' = COS ? w : -w, w, sel) and the select is one PRMT with sel taken
+//    from the record, so COS and SIN butterflies mix in a warp without
+//    divergence:
+//        x = sel(b.re, b.im)  y = sel(b.im, b.re)
+//        u1 = fma(-t, y, x)   u2 = fma(t, x, y)
+//        A = (fma(u1, w', a.re), fma(u2, w, a.im))
+//        B = (fma(-u1, w', a.re), fma(-u2, w, a.im))
+//    Bit-identical to the reference (sign flips are exact; IEEE fma depends
+//    only on the exact product and the addend).
+//  * standard (butterfly.cpp:37-53): 4 mul + 6 add/sub, each rounded
+//    separately (mul.rn/add.rn/sub.rn, __fmul_rn/__fadd_rn/__fsub_rn).
+//  * FP16 packs the same sample of two transforms in one f16x2 register
+//    ((re0,re1), (im0,im1)); every HFMA2 is one correctly rounded binary16 FMA
+//    per lane == ArithmeticContext::fma at fp16 (precision.cpp:98-111).
+//  * FP32 uses FFMA == std::fmaf.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "schedule.cuh"
+
+namespace dsfft {
+
+struct KernelParams {
+  const uint8_t* in;
+  uint8_t* out;
+  const uint4* tw;        // per-stage packed twiddle records (global)
+  long long n_items;      // items = ceil(batch / transforms_per_item)
+  long long batch;        // real transforms
+  uint32_t scale;         // inverse: 1/n as f32 bits or f16x2 (s, s)
+  int stages;             // S: item buffers per group
+};
+
+// ---- arithmetic back ends ---------------------------------------------------
+struct ArithF16 {
+  static constexpr bool kF16 = true;
+  __device__ __forceinline__ static uint32_t fma(uint32_t a, uint32_t b, uint32_t c) {
+    return ptx::hfma2(a, b, c);
+  }
+  __device__ __forceinline__ static uint32_t neg(uint32_t a) { return ptx::hneg2(a); }
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) { return ptx::hadd2(a, b); }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) { return ptx::hsub2(a, b); }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) { return ptx::hmul2(a, b); }
+};
+
+struct ArithF32 {
+  static constexpr bool kF16 = false;
+  __device__ __forceinline__ static float f(uint32_t a) { return __uint_as_float(a); }
+  __device__ __forceinline__ static uint32_t u(float a) { return __float_as_uint(a); }
+  __device__ __forceinline__ static uint32_t fma(uint32_t a, uint32_t b, uint32_t c) {
+    return u(__fmaf_rn(f(a), f(b), f(c)));
+  }
+  __device__ __forceinline__ static uint32_t neg(uint32_t a) { return a ^ 0x80000000u; }
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) { return u(__fadd_rn(f(a), f(b))); }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) { return u(__fsub_rn(f(a), f(b))); }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) { return u(__fmul_rn(f(a), f(b))); }
+};
+
+// One radix-2 butterfly, A = a + W b, B = a - W b, on (re, im) registers.
+template <class A, bool STANDARD>
+__device__ __forceinline__ void butterfly(uint32_t are, uint32_t aim, uint32_t bre,
+                                          uint32_t bim, const uint4& tw, uint32_t& Are,
+                                          uint32_t& Aim, uint32_t& Bre, uint32_t& Bim) {
+  if constexpr (STANDARD) {
+    // record: (omega_r, omega_i, -, -)
+    const uint32_t rr = A::mul(tw.x, bre);
+    const uint32_t ii = A::mul(tw.y, bim);
+    const uint32_t ir = A::mul(tw.y, bre);
+    const uint32_t ri = A::mul(tw.x, bim);
+    const uint32_t tr = A::sub(rr, ii);
+    const uint32_t ti = A::add(ir, ri);
+    Are = A::add(are, tr);
+    Aim = A::add(aim, ti);
+    Bre = A::sub(are, tr);
+    Bim = A::sub(aim, ti);
+  } else {
+    // record: (t, w', w, sel)
+    const uint32_t x = __byte_perm(bre, bim, tw.w);
+    const uint32_t y = __byte_perm(bim, bre, tw.w);
+    const uint32_t u1 = A::fma(A::neg(tw.x), y, x);
+    const uint32_t u2 = A::fma(tw.x, x, y);
+    Are = A::fma(u1, tw.y, are);
+    Aim = A::fma(u2, tw.z, aim);
+    Bre = A::fma(A::neg(u1), tw.y, are);
+    Bim = A::fma(A::neg(u2), tw.z, aim);
+  }
+}
+
+// All local passes of stage ST on the thread's E values.
+template <class Cfg, int ST, class A, bool STANDARD>
+__device__ __forceinline__ void run_stage(uint32_t (&re)[Cfg::E], uint32_t (&im)[Cfg::E],
+                                          uint32_t tw_base, int t) {
+  constexpr int m = Cfg::LOG_N, s = Cfg::s(ST), P = Cfg::P(ST);
+  constexpr int E = Cfg::E, NGRP = E >> s, H = 1 << (s - 1);
+  constexpr bool kSharedR = (Cfg::T % (1 << P)) == 0;  // r independent of j
+  const uint32_t tws = tw_base + Cfg::tw_off(ST) * 16;
+#pragma unroll
+  for (int pl = 0; pl < s; ++pl) {
+    uint32_t nre[E], nim[E];
+#pragma unroll
+    for (int rl = 0; rl < (1 << pl); ++rl) {
+      uint4 tw{};
+      if constexpr (kSharedR) tw = ptx::lds128(tws + tw_slot(P, grp_r(m, P, s, t), pl, rl) * 16);
+#pragma unroll
+      for (int j = 0; j < NGRP; ++j) {
+        if constexpr (!kSharedR)
+          tw = ptx::lds128(tws + tw_slot(P, grp_r(m, P, s, t + Cfg::T * j), pl, rl) * 16);
+#pragma unroll
+        for (int q = 0; q < (H >> pl); ++q) {
+          const int jl = (q << pl) | rl;
+          const int ia = (j << s) + jl, ib = ia + H;
+          const int oa = (j << s) + (q << (pl + 1)) + rl, ob = oa + (1 << pl);
+          butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa], nre[ob],
+                                 nim[ob]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      re[i] = nre[i];
+      im[i] = nim[i];
+    }
+  }
+}
+
+// Gather stage ST's inputs from the padded exchange layout.
+template <class Cfg, int ST>
+__device__ __forceinline__ void read_exchange(uint32_t (&re)[Cfg::E], uint32_t (&im)[Cfg::E],
+                                              uint32_t buf, int t) {
+  constexpr int m = Cfg::LOG_N, s = Cfg::s(ST), P = Cfg::P(ST);
+#pragma unroll
+  for (int j = 0; j < (Cfg::E >> s); ++j)
+#pragma unroll
+    for (int c = 0; c < (1 << s); ++c)
+      ptx::lds64(buf + pad_pos(read_pos(m, P, s, t + Cfg::T * j, c)) * 8, re[(j << s) + c],
+                 im[(j << s) + c]);
+}
+
+// Scatter stage ST's outputs into the padded exchange layout.
+template <class Cfg, int ST>
+__device__ __forceinline__ void write_exchange(const uint32_t (&re)[Cfg::E],
+                                               const uint32_t (&im)[Cfg::E], uint32_t buf,
+                                               int t) {
+  constexpr int m = Cfg::LOG_N, s = Cfg::s(ST), P = Cfg::P(ST);
+#pragma unroll
+  for (int j = 0; j < (Cfg::E >> s); ++j)
+#pragma unroll
+    for (int c = 0; c < (1 << s); ++c)
+      ptx::sts64(buf + pad_pos(write_pos(m, P, s, t + Cfg::T * j, c)) * 8, re[(j << s) + c],
+                 im[(j << s) + c]);
+}
+
+template <class Cfg>
+__device__ __forceinline__ void group_sync(int gid) {
+  if constexpr (Cfg::W == 1) {
+    __syncwarp();
+  } else {
+    ptx::named_bar_sync(1 + gid, Cfg::T);
+  }
+}
+
+template <class Cfg, int ST, class A, bool STANDARD>
+__device__ __forceinline__ void later_stages(uint32_t (&re)[Cfg::E], uint32_t (&im)[Cfg::E],
+                                             uint32_t buf, uint32_t tw_base, int t, int gid) {
+  if constexpr (ST < Cfg::NSTAGE) {
+    group_sync<Cfg>(gid);  // every read of the previous layout is done
+    write_exchange<Cfg, ST - 1>(re, im, buf, t);
+    group_sync<Cfg>(gid);
+    read_exchange<Cfg, ST>(re, im, buf, t);
+    run_stage<Cfg, ST, A, STANDARD>(re, im, tw_base, t);
+    later_stages<Cfg, ST + 1, A, STANDARD>(re, im, buf, tw_base, t, gid);
+  }
+}
+
+// Transform one item resident in smem (natural order in, natural order out).
+template <class Cfg, class A, bool STANDARD, bool INVERSE>
+__device__ __forceinline__ void transform_item(uint32_t buf, uint32_t tw_base, int t, int gid,
+                                               uint32_t scale) {
+  constexpr int m = Cfg::LOG_N, N = Cfg::N, E = Cfg::E;
+  constexpr int s0 = Cfg::s(0), L = Cfg::NSTAGE - 1, sL = Cfg::s(L), PL = Cfg::P(L);
+  uint32_t re[E], im[E];
+  // ---- stage 0 gather from the natural (identity) layout -------------------
+#pragma unroll
+  for (int j = 0; j < (E >> s0); ++j)
+#pragma unroll
+    for (int c = 0; c < (1 << s0); ++c) {
+      const int pos = read_pos(m, 0, s0, t + Cfg::T * j, c);
+      const int v = (j << s0) + c;
+      if constexpr (A::kF16) {
+        const int k = pos >> m, p = pos & (N - 1);
+        const uint32_t lo = ptx::lds32(buf + ((2 * k) * N + p) * 4);
+        const uint32_t hi = ptx::lds32(buf + ((2 * k + 1) * N + p) * 4);
+        re[v] = __byte_perm(lo, hi, 0x5410);
+        im[v] = __byte_perm(lo, hi, 0x7632);
+      } else {
+        ptx::lds64(buf + pos * 8, re[v], im[v]);
+      }
+      if constexpr (INVERSE) im[v] = A::neg(im[v]);  // conj on load (fft.cpp:90-91)
+    }
+  run_stage<Cfg, 0, A, STANDARD>(re, im, tw_base, t);
+  later_stages<Cfg, 1, A, STANDARD>(re, im, buf, tw_base, t, gid);
+  group_sync<Cfg>(gid);
+  // ---- last stage scatter to the natural layout ----------------------------
+#pragma unroll
+  for (int j = 0; j < (E >> sL); ++j)
+#pragma unroll
+    for (int c = 0; c < (1 << sL); ++c) {
+      const int pos = write_pos(m, PL, sL, t + Cfg::T * j, c);
+      const int v = (j << sL) + c;
+      uint32_t xr = re[v], xi = im[v];
+      if constexpr (INVERSE) {  // conj + scale, one rounded mul each (fft.cpp:94-98)
+        xr = A::mul(xr, scale);
+        xi = A::mul(A::neg(xi), scale);
+      }
+      if constexpr (A::kF16) {
+        const int k = pos >> m, p = pos & (N - 1);
+        ptx::sts32(buf + ((2 * k) * N + p) * 4, __byte_perm(xr, xi, 0x5410));
+        ptx::sts32(buf + ((2 * k + 1) * N + p) * 4, __byte_perm(xr, xi, 0x7632));
+      } else {
+        ptx::sts64(buf + pos * 8, xr, xi);
+      }
+    }
+}
+
+template <class Cfg>
+struct SmallLayout {
+  static constexpr int kBufBytes = Cfg::BUF_VALS * 8;
+  static constexpr int kItemBytes = Cfg::VALS * 8;
+  static constexpr int kTwBytes = Cfg::TW_RECORDS * 16;
+  static size_t smem_bytes(int groups, int stages) {
+    return size_t(kTwBytes) + size_t(groups) * stages * kBufBytes + size_t(groups) * stages * 8;
+  }
+};
+
+// Persistent batched FFT over items.  blockDim = NG * T threads.
+template <class Cfg, bool F16, bool STANDARD, bool INVERSE>
+__global__ void __launch_bounds__(Cfg::MAX_THREADS, 1) fft_small_kernel(const KernelParams p) {
+  using A = typename std::conditional<F16, ArithF16, ArithF32>::type;
+  using Lay = SmallLayout<Cfg>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int ng = blockDim.x / Cfg::T;
+  const int gid = threadIdx.x / Cfg::T;
+  const int t = threadIdx.x % Cfg::T;
+  const int S = p.stages;
+  const uint32_t tw_base = ptx::smem_u32(smem);
+  uint8_t* bufs = smem + Lay::kTwBytes + size_t(gid) * S * Lay::kBufBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::kTwBytes +
+                                               size_t(ng) * S * Lay::kBufBytes) +
+                   gid * S;
+  // twiddle records -> smem (once per persistent CTA)
+  for (int i = threadIdx.x; i < Cfg::TW_RECORDS; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = p.tw[i];
+  if (t == 0)
+    for (int b = 0; b < S; ++b) ptx::mbar_init(&bars[b], 1);
+  ptx::fence_mbar_init();
+  __syncthreads();
+
+  constexpr long long kTpi = F16 ? 2LL * Cfg::K : Cfg::K;  // real transforms per item
+  constexpr long long kTb = Cfg::N * (F16 ? 4 : 8);       // bytes per transform
+  const long long first = (long long)blockIdx.x * ng + gid;
+  const long long stride = (long long)gridDim.x * ng;
+  const bool leader = (t == 0);
+  uint64_t pol = 0;
+  if (leader) pol = ptx::policy_evict_first();
+  auto item_bytes = [&](long long item) -> uint32_t {
+    const long long left = p.batch - item * kTpi;
+    return uint32_t((left < kTpi ? left : kTpi) * kTb);
+  };
+  auto issue_load = [&](long long item, int b) {
+    const uint32_t bytes = item_bytes(item);
+    ptx::mbar_arrive_expect_tx(&bars[b], bytes);
+    ptx::bulk_g2s(bufs + size_t(b) * Lay::kBufBytes, p.in + item * Lay::kItemBytes, bytes,
+                  &bars[b], pol);
+  };
+  if (leader)
+    for (int b = 0; b < S; ++b) {
+      const long long item = first + b * stride;
+      if (item < p.n_items) issue_load(item, b);
+    }
+  int it = 0;
+  for (long long item = first; item < p.n_items; item += stride, ++it) {
+    const int b = it % S;
+    ptx::mbar_wait(&bars[b], (it / S) & 1);
+    uint8_t* bp = bufs + size_t(b) * Lay::kBufBytes;
+    transform_item<Cfg, A, STANDARD, INVERSE>(ptx::smem_u32(bp), tw_base, t, gid, p.scale);
+    ptx::fence_proxy_async_smem();
+    group_sync<Cfg>(gid);
+    if (leader) {
+      ptx::bulk_s2g(p.out + item * Lay::kItemBytes, bp, item_bytes(item), pol);
+      ptx::bulk_commit();
+      if (it >= 1) {
+        // the previous item's store has left smem: refill that buffer
+        ptx::bulk_wait_read<1>();
+        const long long nxt = item + (long long)(S - 1) * stride;
+        if (nxt < p.n_items) issue_load(nxt, (it - 1) % S);
+      }
+    }
+  }
+  if (leader) ptx::bulk_wait<0>();
+}
+
+}  // namespace dsfft

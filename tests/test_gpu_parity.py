@@ -1,0 +1,144 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the reference algorithm.
+
+Bar (BASELINE.json north_star): fp32 bit-exact against the reference's own
+fp32 path; fp16 within 2 binary16 ULP per output -- asserted here as
+bit-exact, which the kernels achieve (every HFMA2 is the reference's single
+rounding).  NaN payloads are compared as "both NaN".
+Oracle: oracle/fmafft_oracle.c (pinned to the reference in test_oracle.py),
+or the reference library itself when oracle/_ref was built.
+"""
+import numpy as np
+import pytest
+
+from helpers import ALL_STRATEGIES, WORK_DTYPE, bit_mismatches, max_ulp_fp16, ref_inputs, to_work
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [2 ** m for m in range(1, 13)]
+
+
+def _checker():
+    import oracle
+    return oracle.load_ref() if oracle.ref_available() else oracle.load_oracle()
+
+
+def _device_run(dsfft, torch, plan, xw: np.ndarray, inverse: bool) -> np.ndarray:
+    t = torch.from_numpy(np.ascontiguousarray(xw)).cuda()
+    y = dsfft.execute(plan, 1 if inverse else 0, t)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def _batch_for(n: int) -> int:
+    return max(3, 65536 // n) + 1  # odd: exercises partial items / fp16 pair tails
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+@pytest.mark.parametrize("strategy", ALL_STRATEGIES)
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
+def test_bit_exact_vs_reference(dsfft, cuda, orc, n, strategy, precision, inverse):
+    chk = _checker()
+    batch = _batch_for(n)
+    x = ref_inputs(orc, n, batch, seed=1000 + n, precision=precision)
+    plan = dsfft.make_plan(n, strategy, precision)
+    y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+    want = (chk.inverse if inverse else chk.forward)(x, strategy, precision)
+    want_w = to_work(want, precision)
+    bad = bit_mismatches(y, want_w)
+    if precision == "fp16":
+        assert max_ulp_fp16(y, want_w) <= 2  # the stated tolerance
+    assert bad == 0, f"{bad} of {y.size} components differ"
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_many_items_per_group(dsfft, cuda, orc, precision):
+    """Enough transforms that every persistent group cycles its buffer ring
+    several times; spot-check a strided subset against the oracle."""
+    chk = _checker()
+    n = 1024
+    batch = 148 * 16 * 2 * 3 + 5
+    x = ref_inputs(orc, n, batch, seed=77, precision=precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = _device_run(dsfft, cuda, plan, to_work(x, precision), False)
+    idx = np.r_[0:8, batch - 8:batch, 8:batch - 8:97]
+    want = chk.forward(x[idx], "dual", precision)
+    assert bit_mismatches(y[idx], to_work(want, precision)) == 0
+
+
+def test_in_place_and_streams(dsfft, cuda, orc):
+    torch = cuda
+    n = 1024
+    x = ref_inputs(orc, n, 64, seed=5, precision="fp16")
+    plan = dsfft.make_plan(n, "dual", "fp16")
+    t = torch.from_numpy(to_work(x, "fp16")).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dsfft.forward(plan, t, out=t, stream=s.cuda_stream)
+    s.synchronize()
+    want = to_work(_checker().forward(x, "dual", "fp16"), "fp16")
+    assert bit_mismatches(t.cpu().numpy(), want) == 0
+
+
+def test_host_buffer_paths(dsfft, cuda, orc):
+    """dsfft_execute_host (working precision) and dsfft_execute_f64 (the
+    reference's double-carrier convention with ingest rounding)."""
+    n = 256
+    chk = _checker()
+    raw = orc.random_buffer(n, 9, batch=301)  # unrounded doubles
+    plan = dsfft.make_plan(n, "dual", "fp32")
+    got = dsfft.forward_f64(plan, raw)
+    want = chk.forward(raw, "dual", "fp32")  # forward rounds on ingest (fft.cpp:79-82)
+    assert got.tobytes() == want.tobytes()
+    xw = to_work(ref_inputs(orc, n, 301, 9, "fp32"), "fp32")
+    out = np.empty_like(xw)
+    dsfft.execute_host(plan, 0, xw, out, 301)
+    assert bit_mismatches(out, to_work(want, "fp32")) == 0
+    back = dsfft.inverse_f64(plan, got)
+    assert back.tobytes() == chk.inverse(got, "dual", "fp32").tobytes()
+
+
+def test_nonfinite_propagates(dsfft, cuda, orc):
+    """test_fft.cpp:252-262: NaN input propagates; cosine fp16 is non-finite."""
+    n = 8
+    plan = dsfft.make_plan(n, "dual", "fp16")
+    x = np.ones((1, n), dtype=np.complex128)
+    x[0, 3] = complex(np.nan, 0.0)
+    y = dsfft.forward_f64(plan, x)
+    assert np.isnan(y).any()
+    chk = _checker()
+    xr = ref_inputs(orc, 1024, 4, 3, "fp16")
+    plan = dsfft.make_plan(1024, "cosine", "fp16")
+    y = _device_run(dsfft, cuda, plan, to_work(xr, "fp16"), False)
+    assert not np.isfinite(y).all()
+    assert bit_mismatches(y, to_work(chk.forward(xr, "cosine", "fp16"), "fp16")) == 0
+
+
+def test_signed_zero_and_specials(dsfft, cuda, orc):
+    chk = _checker()
+    n = 64
+    x = np.zeros((4, n), dtype=np.complex128)
+    x[1] = -0.0
+    x[2, ::3] = complex(-0.0, 0.0)
+    x[3, 5] = complex(np.inf, -np.inf)
+    for p in ("fp16", "fp32"):
+        for s in ALL_STRATEGIES:
+            plan = dsfft.make_plan(n, s, p)
+            y = _device_run(dsfft, cuda, plan, to_work(x, p), False)
+            assert bit_mismatches(y, to_work(chk.forward(x, s, p), p)) == 0, (p, s)
+
+
+def test_errors(dsfft, cuda):
+    with pytest.raises(ValueError, match="power of two"):
+        dsfft.make_plan(1023, "dual", "fp16")
+    with pytest.raises(ValueError, match="exceeds 2\\^24"):
+        dsfft.make_plan(1 << 25, "dual", "fp16")
+    with pytest.raises(ValueError, match="clamp_eps"):
+        dsfft.make_plan(8, "lf", "fp32", clamp_eps=0.0)
+    plan = dsfft.make_plan(64, "dual", "fp32")
+    bad = cuda.zeros((2, 32, 2), dtype=cuda.float32, device="cuda")
+    with pytest.raises(ValueError, match="does not match plan size"):
+        dsfft.forward(plan, bad)
+    p64 = dsfft.make_plan(64, "dual", "fp64")
+    with pytest.raises(NotImplementedError):
+        dsfft.forward_f64(p64, np.zeros(64, dtype=np.complex128))
