@@ -95,7 +95,8 @@ struct dsfft_plan_s {
   double clamp_eps = 1e-7;
   std::vector<dsfft::TableEntry> table;  // rounded (FftPlan::table)
   // single-kernel path (m <= 12)
-  const dsfft::SmallEntry* small = nullptr;
+  const dsfft::SmallVariant* small = nullptr;
+  int variant = 0;  // dsfft::SmallVariantId
   uint4* d_tw = nullptr;
   int groups = 0, stages = 0, grid = 0;
   // multi-pass path (m > 12)
@@ -124,10 +125,10 @@ uint32_t inverse_scale_word(const dsfft_plan_s* p) {
 }
 
 // Choose groups per CTA and buffers per group for the single-kernel path.
-void choose_small_launch(dsfft_plan_s* p) {
+void choose_small_launch(dsfft_plan_s* p, int default_stages) {
   const dsfft::SmallGeom& g = p->small->geom;
   const int T = 32 * g.warps;
-  int stages = env_int("DSFFT_STAGES", 3);
+  int stages = env_int("DSFFT_STAGES", default_stages);
   stages = std::max(2, std::min(stages, 8));
   int max_groups = std::max(1, g.max_threads / T);
   int want = env_int("DSFFT_GROUPS", 0);
@@ -159,7 +160,8 @@ int upload_small_tables(dsfft_plan_s* p) {
         for (int r = 0; r < (1 << P); ++r) {
           const int slot = g.tw_off[st] + dsfft::tw_slot(P, r, pl, rl);
           const int k = dsfft::tw_entry(int(p->m), P, r, pl, rl);
-          rec[slot] = dsfft::pack_record(p->table[k], p->strategy, p->precision);
+          rec[slot] = dsfft::pack_record(p->table[k], p->strategy, p->precision,
+                                         p->variant == dsfft::kVarF16C);
         }
   }
   DSFFT_CUDA(cudaMalloc(&p->d_tw, rec.size() * sizeof(dsfft::Record)));
@@ -172,7 +174,6 @@ int upload_small_tables(dsfft_plan_s* p) {
 int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
            cudaStream_t stream) {
   if (batch == 0) return DSFFT_OK;
-  const bool f16 = p->precision == DSFFT_FP16;
   const uint32_t scale = inverse_scale_word(p);
   if (p->mp) {
     const int e = dsfft::multipass_execute(*p->mp, dir == DSFFT_INVERSE, in, out, batch, scale,
@@ -182,14 +183,13 @@ int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
   }
   const dsfft::SmallGeom& g = p->small->geom;
   const size_t tb = p->n * sample_bytes(p->precision);
-  const long long tpi = (f16 ? 2LL : 1LL) * g.k;
+  const long long tpi = g.tpi;
   // bulk copies move multiples of 16 bytes: N=2 fp16 with an odd batch
   // stages its last transform through a padded scratch buffer
   size_t main_batch = batch;
   if ((batch * tb) % 16 != 0) main_batch = batch - 1;
   if (main_batch) {
     dsfft::LaunchArgs a{};
-    a.f16 = f16;
     a.standard = p->strategy == DSFFT_STANDARD;
     a.inverse = dir == DSFFT_INVERSE;
     a.kp.in = static_cast<const uint8_t*>(in);
@@ -212,7 +212,6 @@ int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
     DSFFT_CUDA(cudaMemcpyAsync(p->scratch, static_cast<const uint8_t*>(in) + off, tb,
                                cudaMemcpyDeviceToDevice, stream));
     dsfft::LaunchArgs a{};
-    a.f16 = f16;
     a.standard = p->strategy == DSFFT_STANDARD;
     a.inverse = dir == DSFFT_INVERSE;
     a.kp.in = p->scratch;
@@ -302,8 +301,14 @@ int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, i
   DeviceGuard guard(device);
   int rc = DSFFT_OK;
   if (p->m <= 12) {
-    p->small = &small_entry(int(p->m));
-    choose_small_launch(p);
+    const dsfft::SmallEntry& se = small_entry(int(p->m));
+    p->variant = dsfft::kVarF32;
+    if (precision == DSFFT_FP16) {
+      const int want = env_int("DSFFT_F16_LAYOUT", -1);  // 1 pairs, 2 complex
+      p->variant = (want == dsfft::kVarF16P || want == dsfft::kVarF16C) ? want : se.f16_default;
+    }
+    p->small = &se.v[p->variant];
+    choose_small_launch(p, se.stages[p->variant]);
     rc = upload_small_tables(p);
   } else {
     p->mp = dsfft::multipass_create(p->table, int(p->m), strategy, precision, p->sm_count,

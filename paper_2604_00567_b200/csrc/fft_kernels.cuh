@@ -1,22 +1,23 @@
 // fft_kernels.cuh -- the batched single-kernel radix-2 Stockham FFT for sm_100a.
 //
 // One persistent CTA per SM runs NG independent thread groups; each group owns
-// an S-deep ring of item buffers in shared memory.  Per item (K transforms,
-// 8 KiB at N=1024 FP16):
+// an S-deep ring of item buffers in shared memory.  Per item (K transforms):
 //   TMA bulk load (cp.async.bulk, mbarrier complete_tx)  -> smem
 //   stage 0: gather 2^s0 values per group into registers, s0 passes in regs
-//   exchange through padded smem (conflict-free, schedule_check.cpp)
+//   exchange through padded smem (conflict-free, tools/schedule_check.cpp)
 //   stage 1..: same, the last log2(E) passes entirely in registers
-//   natural-order result -> smem -> TMA bulk store (bulk_group)
-// Loads for the next S-1 items are in flight while an item is computed.
+//   the buffer is released to the next TMA load right after the item's last
+//   smem read; the last stage stores its natural-order results straight
+//   from registers (each warp store covers whole 128-byte lines)
+// Loads for the next S items are in flight while an item is computed.
 //
 // Arithmetic (the parity contract):
 //  * FMA strategies (LF, cosine, dual) use the branch-free unified form of
 //    cosine_core/sine_core (butterfly.cpp:10-33): the host packs per twiddle
-//    (t, w' = COS ? w : -w, w, sel) and the select is one PRMT with sel taken
-//    from the record, so COS and SIN butterflies mix in a warp without
-//    divergence:
-//        x = sel(b.re, b.im)  y = sel(b.im, b.re)
+//    (t, w' = COS ? w : -w, w, selector) and the COS/SIN operand swap is one
+//    PRMT whose selector comes from the record, so COS and SIN butterflies
+//    mix inside a warp without divergence:
+//        (x, y) = COS ? (b.re, b.im) : (b.im, b.re)
 //        u1 = fma(-t, y, x)   u2 = fma(t, x, y)
 //        A = (fma(u1, w', a.re), fma(u2, w, a.im))
 //        B = (fma(-u1, w', a.re), fma(-u2, w, a.im))
@@ -24,12 +25,19 @@
 //    only on the exact product and the addend).
 //  * standard (butterfly.cpp:37-53): 4 mul + 6 add/sub, each rounded
 //    separately (mul.rn/add.rn/sub.rn, __fmul_rn/__fadd_rn/__fsub_rn).
-//  * FP16 packs the same sample of two transforms in one f16x2 register
-//    ((re0,re1), (im0,im1)); every HFMA2 is one correctly rounded binary16 FMA
-//    per lane == ArithmeticContext::fma at fp16 (precision.cpp:98-111).
-//  * FP32 uses FFMA == std::fmaf.
+//  * FP32 (ArithF32): a value is one complex, (re, im) in two registers; FFMA
+//    == std::fmaf.
+//  * FP16, two layouts; every HFMA2 lane is one correctly rounded binary16
+//    FMA == ArithmeticContext::fma at fp16 (precision.cpp:98-111):
+//      ArithF16P  a value is the same sample of two transforms,
+//                 (re0,re1),(im0,im1): 6 HFMA2 + 2 PRMT per 2 butterflies;
+//      ArithF16C  a value is one complex (re,im) in one f16x2 register:
+//                 u = fma((-t,t), (y,x), (x,y)); A = fma(u, (w',w), a);
+//                 B = fma(u, -(w',w), a): 3 HFMA2 + 2 PRMT per butterfly,
+//                 half the registers and buffer bytes per transform.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "schedule.cuh"
@@ -47,8 +55,7 @@ struct KernelParams {
 };
 
 // ---- arithmetic back ends ---------------------------------------------------
-struct ArithF16 {
-  static constexpr bool kF16 = true;
+struct F16Ops {
   __device__ __forceinline__ static uint32_t fma(uint32_t a, uint32_t b, uint32_t c) {
     return ptx::hfma2(a, b, c);
   }
@@ -58,8 +65,18 @@ struct ArithF16 {
   __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) { return ptx::hmul2(a, b); }
 };
 
+// FP16, transform pairs: two words per value, two real transforms per
+// virtual transform.
+struct ArithF16P : F16Ops {
+  static constexpr int kWords = 2, kPair = 2, kSampleBytes = 4;
+};
+// FP16, one complex per register.
+struct ArithF16C : F16Ops {
+  static constexpr int kWords = 1, kPair = 1, kSampleBytes = 4;
+};
+
 struct ArithF32 {
-  static constexpr bool kF16 = false;
+  static constexpr int kWords = 2, kPair = 1, kSampleBytes = 8;
   __device__ __forceinline__ static float f(uint32_t a) { return __uint_as_float(a); }
   __device__ __forceinline__ static uint32_t u(float a) { return __float_as_uint(a); }
   __device__ __forceinline__ static uint32_t fma(uint32_t a, uint32_t b, uint32_t c) {
@@ -71,12 +88,43 @@ struct ArithF32 {
   __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) { return u(__fmul_rn(f(a), f(b))); }
 };
 
-// One radix-2 butterfly, A = a + W b, B = a - W b, on (re, im) registers.
+// Bytes of one stored value (one complex or one transform-pair sample).
+template <class A>
+__host__ __device__ constexpr int value_bytes() { return A::kWords * 4; }
+
+// CTA size cap (sets the register budget): 2E data registers for two-word
+// values (E=32 -> 128 regs, 512 threads), E for one-word values.
+template <class Cfg, class A>
+__host__ __device__ constexpr int max_threads() {
+  return A::kWords == 2 ? (Cfg::LOG_E >= 6 ? 256 : 512) : (Cfg::LOG_E >= 6 ? 512 : 768);
+}
+
+// One radix-2 butterfly, A = a + W b, B = a - W b.
+//   two-word values: (re, im) registers; one-word: f16x2 (re, im) in `re`.
 template <class A, bool STANDARD>
 __device__ __forceinline__ void butterfly(uint32_t are, uint32_t aim, uint32_t bre,
                                           uint32_t bim, const uint4& tw, uint32_t& Are,
                                           uint32_t& Aim, uint32_t& Bre, uint32_t& Bim) {
-  if constexpr (STANDARD) {
+  if constexpr (A::kWords == 1) {
+    if constexpr (STANDARD) {
+      // record: ((wr, wi), (wi, wr), -, -)
+      const uint32_t rr_ii = A::mul(bre, tw.x);  // (wr*br, wi*bi)
+      const uint32_t ir_ri = A::mul(bre, tw.y);  // (wi*br, wr*bi)
+      const uint32_t p = __byte_perm(rr_ii, ir_ri, 0x5410);  // (rr, ir)
+      const uint32_t q = __byte_perm(rr_ii, ir_ri, 0x7632);  // (ii, ri)
+      // (rr - ii, ir + ri): fma by -1 / +1 is one exact-product rounding
+      const uint32_t t = A::fma(q, 0x3C00BC00u, p);
+      Are = A::add(are, t);
+      Bre = A::sub(are, t);
+    } else {
+      // record: ((-t, t), (w', w), sel_xy, sel_yx)
+      const uint32_t xy = __byte_perm(bre, bre, tw.z);
+      const uint32_t yx = __byte_perm(bre, bre, tw.w);
+      const uint32_t u = A::fma(tw.x, yx, xy);
+      Are = A::fma(u, tw.y, are);
+      Bre = A::fma(u, A::neg(tw.y), are);
+    }
+  } else if constexpr (STANDARD) {
     // record: (omega_r, omega_i, -, -)
     const uint32_t rr = A::mul(tw.x, bre);
     const uint32_t ii = A::mul(tw.y, bim);
@@ -133,26 +181,30 @@ __device__ __forceinline__ void run_stage(uint32_t (&re)[Cfg::E], uint32_t (&im)
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       re[i] = nre[i];
-      im[i] = nim[i];
+      if constexpr (A::kWords == 2) im[i] = nim[i];
     }
   }
 }
 
 // Gather stage ST's inputs from the padded exchange layout.
-template <class Cfg, int ST>
+template <class Cfg, int ST, class A>
 __device__ __forceinline__ void read_exchange(uint32_t (&re)[Cfg::E], uint32_t (&im)[Cfg::E],
                                               uint32_t buf, int t) {
   constexpr int m = Cfg::LOG_N, s = Cfg::s(ST), P = Cfg::P(ST);
 #pragma unroll
   for (int j = 0; j < (Cfg::E >> s); ++j)
 #pragma unroll
-    for (int c = 0; c < (1 << s); ++c)
-      ptx::lds64(buf + pad_pos(read_pos(m, P, s, t + Cfg::T * j, c)) * 8, re[(j << s) + c],
-                 im[(j << s) + c]);
+    for (int c = 0; c < (1 << s); ++c) {
+      const uint32_t a = buf + pad_pos(read_pos(m, P, s, t + Cfg::T * j, c)) * value_bytes<A>();
+      if constexpr (A::kWords == 2)
+        ptx::lds64(a, re[(j << s) + c], im[(j << s) + c]);
+      else
+        re[(j << s) + c] = ptx::lds32(a);
+    }
 }
 
 // Scatter stage ST's outputs into the padded exchange layout.
-template <class Cfg, int ST>
+template <class Cfg, int ST, class A>
 __device__ __forceinline__ void write_exchange(const uint32_t (&re)[Cfg::E],
                                                const uint32_t (&im)[Cfg::E], uint32_t buf,
                                                int t) {
@@ -160,9 +212,13 @@ __device__ __forceinline__ void write_exchange(const uint32_t (&re)[Cfg::E],
 #pragma unroll
   for (int j = 0; j < (Cfg::E >> s); ++j)
 #pragma unroll
-    for (int c = 0; c < (1 << s); ++c)
-      ptx::sts64(buf + pad_pos(write_pos(m, P, s, t + Cfg::T * j, c)) * 8, re[(j << s) + c],
-                 im[(j << s) + c]);
+    for (int c = 0; c < (1 << s); ++c) {
+      const uint32_t a = buf + pad_pos(write_pos(m, P, s, t + Cfg::T * j, c)) * value_bytes<A>();
+      if constexpr (A::kWords == 2)
+        ptx::sts64(a, re[(j << s) + c], im[(j << s) + c]);
+      else
+        ptx::sts32(a, re[(j << s) + c]);
+    }
 }
 
 template <class Cfg>
@@ -174,23 +230,30 @@ __device__ __forceinline__ void group_sync(int gid) {
   }
 }
 
-template <class Cfg, int ST, class A, bool STANDARD>
+template <class Cfg, int ST, class A, bool STANDARD, class Release>
 __device__ __forceinline__ void later_stages(uint32_t (&re)[Cfg::E], uint32_t (&im)[Cfg::E],
-                                             uint32_t buf, uint32_t tw_base, int t, int gid) {
+                                             uint32_t buf, uint32_t tw_base, int t, int gid,
+                                             Release& release) {
   if constexpr (ST < Cfg::NSTAGE) {
     group_sync<Cfg>(gid);  // every read of the previous layout is done
-    write_exchange<Cfg, ST - 1>(re, im, buf, t);
+    write_exchange<Cfg, ST - 1, A>(re, im, buf, t);
     group_sync<Cfg>(gid);
-    read_exchange<Cfg, ST>(re, im, buf, t);
+    read_exchange<Cfg, ST, A>(re, im, buf, t);
+    if constexpr (ST == Cfg::NSTAGE - 1) release();  // last smem read of this item
     run_stage<Cfg, ST, A, STANDARD>(re, im, tw_base, t);
-    later_stages<Cfg, ST + 1, A, STANDARD>(re, im, buf, tw_base, t, gid);
+    later_stages<Cfg, ST + 1, A, STANDARD>(re, im, buf, tw_base, t, gid, release);
   }
 }
 
-// Transform one item resident in smem (natural order in, natural order out).
-template <class Cfg, class A, bool STANDARD, bool INVERSE>
+// Transform one item resident in smem (natural order in) and write it to
+// global memory in natural order straight from registers.  `release()` runs
+// as soon as the item's last shared-memory read is done, so the buffer is
+// refilled by TMA while the last stage computes.  `valid` = real transforms
+// of this item that exist (the batch tail).
+template <class Cfg, class A, bool STANDARD, bool INVERSE, class Release>
 __device__ __forceinline__ void transform_item(uint32_t buf, uint32_t tw_base, int t, int gid,
-                                               uint32_t scale) {
+                                               uint32_t scale, uint8_t* gout, int valid,
+                                               Release& release) {
   constexpr int m = Cfg::LOG_N, N = Cfg::N, E = Cfg::E;
   constexpr int s0 = Cfg::s(0), L = Cfg::NSTAGE - 1, sL = Cfg::s(L), PL = Cfg::P(L);
   uint32_t re[E], im[E];
@@ -201,57 +264,74 @@ __device__ __forceinline__ void transform_item(uint32_t buf, uint32_t tw_base, i
     for (int c = 0; c < (1 << s0); ++c) {
       const int pos = read_pos(m, 0, s0, t + Cfg::T * j, c);
       const int v = (j << s0) + c;
-      if constexpr (A::kF16) {
+      if constexpr (A::kPair == 2) {
         const int k = pos >> m, p = pos & (N - 1);
         const uint32_t lo = ptx::lds32(buf + ((2 * k) * N + p) * 4);
         const uint32_t hi = ptx::lds32(buf + ((2 * k + 1) * N + p) * 4);
         re[v] = __byte_perm(lo, hi, 0x5410);
         im[v] = __byte_perm(lo, hi, 0x7632);
-      } else {
+        if constexpr (INVERSE) im[v] = A::neg(im[v]);  // conj on load (fft.cpp:90-91)
+      } else if constexpr (A::kWords == 2) {
         ptx::lds64(buf + pos * 8, re[v], im[v]);
+        if constexpr (INVERSE) im[v] = A::neg(im[v]);
+      } else {
+        re[v] = ptx::lds32(buf + pos * 4);
+        if constexpr (INVERSE) re[v] ^= 0x80000000u;  // negate the im half only
       }
-      if constexpr (INVERSE) im[v] = A::neg(im[v]);  // conj on load (fft.cpp:90-91)
     }
+  if constexpr (Cfg::NSTAGE == 1) release();
   run_stage<Cfg, 0, A, STANDARD>(re, im, tw_base, t);
-  later_stages<Cfg, 1, A, STANDARD>(re, im, buf, tw_base, t, gid);
-  group_sync<Cfg>(gid);
-  // ---- last stage scatter to the natural layout ----------------------------
+  later_stages<Cfg, 1, A, STANDARD>(re, im, buf, tw_base, t, gid, release);
+  // ---- last stage: natural-order stores from registers (coalesced) ---------
 #pragma unroll
   for (int j = 0; j < (E >> sL); ++j)
 #pragma unroll
     for (int c = 0; c < (1 << sL); ++c) {
       const int pos = write_pos(m, PL, sL, t + Cfg::T * j, c);
       const int v = (j << sL) + c;
-      uint32_t xr = re[v], xi = im[v];
-      if constexpr (INVERSE) {  // conj + scale, one rounded mul each (fft.cpp:94-98)
-        xr = A::mul(xr, scale);
-        xi = A::mul(A::neg(xi), scale);
-      }
-      if constexpr (A::kF16) {
-        const int k = pos >> m, p = pos & (N - 1);
-        ptx::sts32(buf + ((2 * k) * N + p) * 4, __byte_perm(xr, xi, 0x5410));
-        ptx::sts32(buf + ((2 * k + 1) * N + p) * 4, __byte_perm(xr, xi, 0x7632));
+      const int k = pos >> m, p = pos & (N - 1);
+      if constexpr (A::kWords == 1) {
+        uint32_t x = re[v];
+        if constexpr (INVERSE)  // (re*s, (-im)*s), one rounded mul each (fft.cpp:94-98)
+          x = A::mul(x ^ 0x80000000u, scale);
+        if (k < valid) __stcs(reinterpret_cast<unsigned int*>(gout + size_t(pos) * 4), x);
       } else {
-        ptx::sts64(buf + pos * 8, xr, xi);
+        uint32_t xr = re[v], xi = im[v];
+        if constexpr (INVERSE) {  // conj + scale, one rounded mul each (fft.cpp:94-98)
+          xr = A::mul(xr, scale);
+          xi = A::mul(A::neg(xi), scale);
+        }
+        if constexpr (A::kPair == 2) {
+          if (2 * k < valid)
+            __stcs(reinterpret_cast<unsigned int*>(gout + (size_t(2 * k) * N + p) * 4),
+                   __byte_perm(xr, xi, 0x5410));
+          if (2 * k + 1 < valid)
+            __stcs(reinterpret_cast<unsigned int*>(gout + (size_t(2 * k + 1) * N + p) * 4),
+                   __byte_perm(xr, xi, 0x7632));
+        } else {
+          if (k < valid)
+            __stcs(reinterpret_cast<uint2*>(gout + size_t(pos) * 8), make_uint2(xr, xi));
+        }
       }
     }
 }
 
-template <class Cfg>
+template <class Cfg, class A>
 struct SmallLayout {
-  static constexpr int kBufBytes = Cfg::BUF_VALS * 8;
-  static constexpr int kItemBytes = Cfg::VALS * 8;
+  static constexpr int kBufBytes = Cfg::BUF_VALS * value_bytes<A>();
+  static constexpr int kItemBytes = Cfg::VALS * value_bytes<A>();
   static constexpr int kTwBytes = Cfg::TW_RECORDS * 16;
+  static constexpr int kTpi = Cfg::K * A::kPair;            // real transforms per item
+  static constexpr int kTb = Cfg::N * A::kSampleBytes;      // bytes per transform
   static size_t smem_bytes(int groups, int stages) {
     return size_t(kTwBytes) + size_t(groups) * stages * kBufBytes + size_t(groups) * stages * 8;
   }
 };
 
 // Persistent batched FFT over items.  blockDim = NG * T threads.
-template <class Cfg, bool F16, bool STANDARD, bool INVERSE>
-__global__ void __launch_bounds__(Cfg::MAX_THREADS, 1) fft_small_kernel(const KernelParams p) {
-  using A = typename std::conditional<F16, ArithF16, ArithF32>::type;
-  using Lay = SmallLayout<Cfg>;
+template <class Cfg, class A, bool STANDARD, bool INVERSE>
+__global__ void __launch_bounds__(max_threads<Cfg, A>(), 1) fft_small_kernel(const KernelParams p) {
+  using Lay = SmallLayout<Cfg, A>;
   extern __shared__ __align__(128) uint8_t smem[];
   const int ng = blockDim.x / Cfg::T;
   const int gid = threadIdx.x / Cfg::T;
@@ -270,19 +350,16 @@ __global__ void __launch_bounds__(Cfg::MAX_THREADS, 1) fft_small_kernel(const Ke
   ptx::fence_mbar_init();
   __syncthreads();
 
-  constexpr long long kTpi = F16 ? 2LL * Cfg::K : Cfg::K;  // real transforms per item
-  constexpr long long kTb = Cfg::N * (F16 ? 4 : 8);       // bytes per transform
+  constexpr long long kTpi = Lay::kTpi;
+  constexpr long long kTb = Lay::kTb;
   const long long first = (long long)blockIdx.x * ng + gid;
   const long long stride = (long long)gridDim.x * ng;
   const bool leader = (t == 0);
   uint64_t pol = 0;
   if (leader) pol = ptx::policy_evict_first();
-  auto item_bytes = [&](long long item) -> uint32_t {
-    const long long left = p.batch - item * kTpi;
-    return uint32_t((left < kTpi ? left : kTpi) * kTb);
-  };
   auto issue_load = [&](long long item, int b) {
-    const uint32_t bytes = item_bytes(item);
+    const long long left = p.batch - item * kTpi;
+    const uint32_t bytes = uint32_t((left < kTpi ? left : kTpi) * kTb);
     ptx::mbar_arrive_expect_tx(&bars[b], bytes);
     ptx::bulk_g2s(bufs + size_t(b) * Lay::kBufBytes, p.in + item * Lay::kItemBytes, bytes,
                   &bars[b], pol);
@@ -297,21 +374,18 @@ __global__ void __launch_bounds__(Cfg::MAX_THREADS, 1) fft_small_kernel(const Ke
     const int b = it % S;
     ptx::mbar_wait(&bars[b], (it / S) & 1);
     uint8_t* bp = bufs + size_t(b) * Lay::kBufBytes;
-    transform_item<Cfg, A, STANDARD, INVERSE>(ptx::smem_u32(bp), tw_base, t, gid, p.scale);
-    ptx::fence_proxy_async_smem();
-    group_sync<Cfg>(gid);
-    if (leader) {
-      ptx::bulk_s2g(p.out + item * Lay::kItemBytes, bp, item_bytes(item), pol);
-      ptx::bulk_commit();
-      if (it >= 1) {
-        // the previous item's store has left smem: refill that buffer
-        ptx::bulk_wait_read<1>();
-        const long long nxt = item + (long long)(S - 1) * stride;
-        if (nxt < p.n_items) issue_load(nxt, (it - 1) % S);
-      }
-    }
+    const long long left = p.batch - item * kTpi;
+    const int valid = int(left < kTpi ? left : kTpi);
+    auto release = [&]() {
+      // all generic-proxy accesses of buffer b precede the next TMA write
+      ptx::fence_proxy_async_smem();
+      group_sync<Cfg>(gid);
+      const long long nxt = item + (long long)S * stride;
+      if (leader && nxt < p.n_items) issue_load(nxt, b);
+    };
+    transform_item<Cfg, A, STANDARD, INVERSE>(ptx::smem_u32(bp), tw_base, t, gid, p.scale,
+                                              p.out + item * Lay::kItemBytes, valid, release);
   }
-  if (leader) ptx::bulk_wait<0>();
 }
 
 }  // namespace dsfft

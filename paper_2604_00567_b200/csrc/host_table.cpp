@@ -165,14 +165,25 @@ void effective_operands(const TableEntry& e, int strategy, double* t, double* w,
   }
 }
 
-Record pack_record(const TableEntry& e, int strategy, int precision) {
+Record pack_record(const TableEntry& e, int strategy, int precision, bool f16_complex) {
+  double t, w;
+  bool cos = true;
+  if (strategy != kStandard) effective_operands(e, strategy, &t, &w, &cos);
+  if (precision == kFp16 && f16_complex) {
+    // one complex per f16x2 register: low half = re lane, high half = im lane
+    auto pair = [](double lo, double hi) -> uint32_t {
+      return uint32_t(half_bits(lo)) | (uint32_t(half_bits(hi)) << 16);
+    };
+    if (strategy == kStandard)
+      return Record{pair(e.omega_r, e.omega_i), pair(e.omega_i, e.omega_r), 0u, 0u};
+    // (-t, t), (w', w), PRMT selectors producing (x, y) and (y, x) from b
+    return Record{pair(-t, t), pair(cos ? w : -w, w), cos ? 0x3210u : 0x1032u,
+                  cos ? 0x1032u : 0x3210u};
+  }
   auto word = [&](double v) -> uint32_t {
     return precision == kFp16 ? dup16(half_bits(v)) : f32_bits(v);
   };
   if (strategy == kStandard) return Record{word(e.omega_r), word(e.omega_i), 0u, 0u};
-  double t, w;
-  bool cos;
-  effective_operands(e, strategy, &t, &w, &cos);
   return Record{word(t), word(cos ? w : -w), word(w), cos ? 0x3210u : 0x7654u};
 }
 

@@ -56,7 +56,8 @@ double round_to(double x, int precision);
 struct Record {
   uint32_t x, y, z, w;
 };
-Record pack_record(const TableEntry& rounded, int strategy, int precision);
+Record pack_record(const TableEntry& rounded, int strategy, int precision,
+                   bool f16_complex = false);
 
 // Effective (t, w, cos?) a butterfly uses for an entry: mirrors the operand
 // choice of butterfly_linzer_feig / butterfly_cosine / butterfly_dual

@@ -1,6 +1,8 @@
 // inst_small.cu -- compiled once per transform size with -DDSFFT_M=<log2 N>;
-// defines small_entry_m<M>() with that size's schedule (see schedule_check.cpp
-// for the dataflow proof and bank-conflict counts of each choice).
+// defines small_entry_m<M>() with that size's schedules (tools/
+// schedule_check.cpp proves each dataflow-exact and counts its bank
+// conflicts).  CfgW: two-word values (fp32 complex, fp16 transform pairs);
+// CfgC: one-word values (fp16 complex in one f16x2 register).
 #include "small_launch.cuh"
 
 #ifndef DSFFT_M
@@ -11,27 +13,47 @@ namespace dsfft {
 
 //            LOG_N LOG_E W  stages (passes per register stage)
 #if DSFFT_M <= 5
-using CfgM = Sched<DSFFT_M, 5, 1, DSFFT_M>;
+using CfgW = Sched<DSFFT_M, 5, 1, DSFFT_M>;
+using CfgC = CfgW;
 #elif DSFFT_M == 6
-using CfgM = Sched<6, 5, 1, 3, 3>;
+using CfgW = Sched<6, 5, 1, 3, 3>;
+using CfgC = CfgW;
 #elif DSFFT_M == 7
-using CfgM = Sched<7, 5, 1, 4, 3>;
+using CfgW = Sched<7, 5, 1, 4, 3>;
+using CfgC = CfgW;
 #elif DSFFT_M == 8
-using CfgM = Sched<8, 5, 1, 4, 4>;
+using CfgW = Sched<8, 5, 1, 4, 4>;
+using CfgC = CfgW;
 #elif DSFFT_M == 9
-using CfgM = Sched<9, 5, 1, 5, 4>;
+using CfgW = Sched<9, 5, 1, 5, 4>;
+using CfgC = CfgW;
 #elif DSFFT_M == 10
-using CfgM = Sched<10, 5, 1, 5, 5>;
+using CfgW = Sched<10, 5, 1, 5, 5>;
+using CfgC = CfgW;
 #elif DSFFT_M == 11
-using CfgM = Sched<11, 6, 1, 5, 6>;
+using CfgW = Sched<11, 6, 1, 5, 6>;
+using CfgC = CfgW;
 #elif DSFFT_M == 12
-using CfgM = Sched<12, 6, 2, 6, 6>;
+using CfgW = Sched<12, 6, 2, 6, 6>;
+using CfgC = CfgW;
 #else
 #error "single-kernel path covers N <= 4096"
 #endif
 
 #define DSFFT_CAT2(a, b) a##b
 #define DSFFT_CAT(a, b) DSFFT_CAT2(a, b)
-SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() { return make_small_entry<CfgM>(); }
+SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
+  SmallEntry e{};
+  e.v[kVarF32] = make_variant<CfgW, ArithF32>();
+  e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
+  e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
+  // B200 sweeps at N=1024 (profiles/README.md): fp16 pairs S=2 x 12 groups
+  // 93% of HBM vs complex-per-register 83%; fp32 S=3 x 8 groups 96%.
+  e.f16_default = kVarF16P;
+  e.stages[kVarF32] = 3;
+  e.stages[kVarF16P] = 2;
+  e.stages[kVarF16C] = 2;
+  return e;
+}
 
 }  // namespace dsfft

@@ -98,8 +98,6 @@ struct Sched {
   }
   static constexpr int TW_RECORDS = tw_off(NSTAGE);
   static constexpr int BUF_VALS = padded_size(VALS);  // 8-byte values
-  // 64 values per thread need ~170 registers: cap the CTA at 256 threads.
-  static constexpr int MAX_THREADS = LOG_E >= 6 ? 256 : 512;
   static_assert(S0 + S1 + S2 + S3 == LOG_N, "stages must cover every pass");
   static_assert(VALS % N == 0, "an item holds whole transforms");
   static_assert(S0 <= LOG_E && S1 <= LOG_E && S2 <= LOG_E && S3 <= LOG_E,

@@ -1,8 +1,9 @@
 // small_launch.cuh -- per-size instantiation and launch of fft_small_kernel.
 //
-// Each csrc/inst_m<M>.cu instantiates the 8 kernels (fp16/fp32 x
-// FMA/standard x forward/inverse) of one transform size M = log2 N, so the
-// heavily unrolled kernels compile in parallel.
+// Each csrc/inst_small.cu object (compiled with -DDSFFT_M=<log2 N>)
+// instantiates the kernels of one transform size for three value layouts
+// (fp32, fp16 transform-pairs, fp16 complex) x {FMA, standard} x {forward,
+// inverse}, so the heavily unrolled kernels compile in parallel.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -12,15 +13,19 @@
 
 namespace dsfft {
 
+enum SmallVariantId : int { kVarF32 = 0, kVarF16P = 1, kVarF16C = 2 };
+
 // Runtime description of a compiled configuration (mirrors Sched<>).
 struct SmallGeom {
   int m, log_e, warps, nstage;
   int s[4], P[4], tw_off[5];
-  int tw_records, vals, k, buf_bytes, item_bytes, max_threads;
+  int tw_records, vals, k, max_threads;
+  int tpi;         // real transforms per item
+  int item_bytes;  // bytes of one item in global memory
 };
 
 struct LaunchArgs {
-  bool f16, standard, inverse;
+  bool standard, inverse;
   KernelParams kp;
   cudaStream_t stream;
   int grid, groups;
@@ -28,13 +33,19 @@ struct LaunchArgs {
 
 using SmallLaunchFn = cudaError_t (*)(const LaunchArgs&);
 
-struct SmallEntry {
+struct SmallVariant {
   SmallGeom geom;
   SmallLaunchFn launch;
   size_t (*smem_bytes)(int groups, int stages);
 };
 
-template <class Cfg>
+struct SmallEntry {
+  SmallVariant v[3];     // indexed by SmallVariantId
+  int f16_default;       // kVarF16P or kVarF16C
+  int stages[3];         // default item buffers per group, per variant (measured)
+};
+
+template <class Cfg, class A>
 SmallGeom make_geom() {
   SmallGeom g{};
   g.m = Cfg::LOG_N;
@@ -49,16 +60,16 @@ SmallGeom make_geom() {
   g.tw_records = Cfg::TW_RECORDS;
   g.vals = Cfg::VALS;
   g.k = Cfg::K;
-  g.buf_bytes = SmallLayout<Cfg>::kBufBytes;
-  g.item_bytes = SmallLayout<Cfg>::kItemBytes;
-  g.max_threads = Cfg::MAX_THREADS;
+  g.max_threads = max_threads<Cfg, A>();
+  g.tpi = SmallLayout<Cfg, A>::kTpi;
+  g.item_bytes = SmallLayout<Cfg, A>::kItemBytes;
   return g;
 }
 
-template <class Cfg, bool F16, bool STD, bool INV>
+template <class Cfg, class A, bool STD, bool INV>
 cudaError_t launch_variant(const LaunchArgs& a) {
-  auto kern = fft_small_kernel<Cfg, F16, STD, INV>;
-  const size_t smem = SmallLayout<Cfg>::smem_bytes(a.groups, a.kp.stages);
+  auto kern = fft_small_kernel<Cfg, A, STD, INV>;
+  const size_t smem = SmallLayout<Cfg, A>::smem_bytes(a.groups, a.kp.stages);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem));
   if (e != cudaSuccess) return e;
@@ -66,33 +77,24 @@ cudaError_t launch_variant(const LaunchArgs& a) {
   return cudaGetLastError();
 }
 
-template <class Cfg>
+template <class Cfg, class A>
 cudaError_t launch_small(const LaunchArgs& a) {
-  if (a.f16) {
-    if (a.standard)
-      return a.inverse ? launch_variant<Cfg, true, true, true>(a)
-                       : launch_variant<Cfg, true, true, false>(a);
-    return a.inverse ? launch_variant<Cfg, true, false, true>(a)
-                     : launch_variant<Cfg, true, false, false>(a);
-  }
   if (a.standard)
-    return a.inverse ? launch_variant<Cfg, false, true, true>(a)
-                     : launch_variant<Cfg, false, true, false>(a);
-  return a.inverse ? launch_variant<Cfg, false, false, true>(a)
-                   : launch_variant<Cfg, false, false, false>(a);
+    return a.inverse ? launch_variant<Cfg, A, true, true>(a) : launch_variant<Cfg, A, true, false>(a);
+  return a.inverse ? launch_variant<Cfg, A, false, true>(a) : launch_variant<Cfg, A, false, false>(a);
 }
 
-template <class Cfg>
+template <class Cfg, class A>
 size_t small_smem_bytes(int groups, int stages) {
-  return SmallLayout<Cfg>::smem_bytes(groups, stages);
+  return SmallLayout<Cfg, A>::smem_bytes(groups, stages);
 }
 
-template <class Cfg>
-SmallEntry make_small_entry() {
-  return SmallEntry{make_geom<Cfg>(), &launch_small<Cfg>, &small_smem_bytes<Cfg>};
+template <class Cfg, class A>
+SmallVariant make_variant() {
+  return SmallVariant{make_geom<Cfg, A>(), &launch_small<Cfg, A>, &small_smem_bytes<Cfg, A>};
 }
 
-// Defined in inst_m<M>.cu
+// Defined in inst_small.cu (one object per M)
 SmallEntry small_entry_m1();
 SmallEntry small_entry_m2();
 SmallEntry small_entry_m3();
