@@ -107,6 +107,15 @@ int dsfft_execute(dsfft_plan plan, int direction, const void* d_in, void* d_out,
 int dsfft_execute_host(dsfft_plan plan, int direction, const void* h_in, void* h_out,
                        size_t batch, void* stream);
 
+/* Batch partitioner over the GPUs of one box: plans[i] is a
+ * plan for device i (same n / strategy / precision); transforms
+ * [i*batch/nplans, (i+1)*batch/nplans) of the host buffers run on device i
+ * through its own dsfft_execute_host pipeline, one host thread per device.
+ * No data crosses devices (no collectives).  The reference has no parallel
+ * path; this extends forward/inverse (fft.hpp:33-39) over devices. */
+int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int direction, const void* h_in,
+                        void* h_out, size_t batch);
+
 /* The reference's exact calling convention: double-carrier SampleBuffers
  * (interleaved re, im doubles, fft.hpp:12).  Rounds on ingest with round_to
  * semantics, runs on the device, widens the result back to double. */

@@ -265,3 +265,15 @@ def widen(raw: np.ndarray, precision: str) -> np.ndarray:
 
 def last_launch_count() -> int:
     return int(_load().dsfft_last_launch_count())
+
+
+def execute_multi(plans, direction: int, h_in: np.ndarray, h_out: np.ndarray,
+                  batch: int) -> None:
+    """Batch partitioner over devices (dsfft_execute_multi): plans[i] runs the
+    contiguous shard i of the host batch on its own device."""
+    lib = _load()
+    lib.dsfft_execute_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                        C.c_size_t]
+    arr = (C.c_void_p * len(plans))(*[p._handle for p in plans])
+    _check(lib.dsfft_execute_multi(C.cast(arr, C.c_void_p), len(plans), direction,
+                                   h_in.ctypes.data, h_out.ctypes.data, batch))

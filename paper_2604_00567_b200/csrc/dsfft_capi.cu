@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dsfft.h"
@@ -433,6 +434,43 @@ int dsfft_execute_host(dsfft_plan p, int dir, const void* h_in, void* h_out, siz
   }
   DSFFT_CUDA(cudaStreamSynchronize(user));
   g_launches = launches;
+  return DSFFT_OK;
+}
+
+int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int dir, const void* h_in,
+                        void* h_out, size_t batch) {
+  g_launches = 0;
+  if (!plans || nplans < 1) return fail(DSFFT_ERR_INVALID, "no plans");
+  for (int i = 0; i < nplans; ++i) {
+    int rc = check_exec_args(plans[i], dir, h_in, h_out);
+    if (rc) return rc;
+    if (plans[i]->n != plans[0]->n || plans[i]->precision != plans[0]->precision ||
+        plans[i]->strategy != plans[0]->strategy)
+      return fail(DSFFT_ERR_INVALID, "plans differ in size, strategy or precision");
+  }
+  const size_t tb = plans[0]->n * sample_bytes(plans[0]->precision);
+  std::vector<int> rcs(nplans, DSFFT_OK);
+  std::vector<std::string> errs(nplans);
+  std::vector<uint64_t> launches(nplans, 0);
+  std::vector<std::thread> pool;
+  for (int i = 0; i < nplans; ++i) {
+    const size_t b0 = batch * size_t(i) / size_t(nplans);
+    const size_t b1 = batch * size_t(i + 1) / size_t(nplans);
+    pool.emplace_back([&, i, b0, b1] {
+      if (b1 == b0) return;
+      rcs[i] = dsfft_execute_host(plans[i], dir, static_cast<const uint8_t*>(h_in) + b0 * tb,
+                                  static_cast<uint8_t*>(h_out) + b0 * tb, b1 - b0, nullptr);
+      errs[i] = g_err;
+      launches[i] = g_launches;
+    });
+  }
+  for (auto& t : pool) t.join();
+  uint64_t total = 0;
+  for (int i = 0; i < nplans; ++i) {
+    if (rcs[i] != DSFFT_OK) return fail(rcs[i], "device " + std::to_string(i) + ": " + errs[i]);
+    total += launches[i];
+  }
+  g_launches = total;
   return DSFFT_OK;
 }
 

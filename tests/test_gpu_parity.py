@@ -142,3 +142,19 @@ def test_errors(dsfft, cuda):
     p64 = dsfft.make_plan(64, "dual", "fp64")
     with pytest.raises(NotImplementedError):
         dsfft.forward_f64(p64, np.zeros(64, dtype=np.complex128))
+
+
+def test_execute_multi_partitioner(dsfft, cuda, orc):
+    """dsfft_execute_multi: contiguous shards on each listed device (here the
+    one B200 twice, two host threads) reproduce the single-call result."""
+    n, batch = 1024, 101
+    x = to_work(ref_inputs(orc, n, batch, 21, "fp16"), "fp16")
+    plans = [dsfft.make_plan(n, "dual", "fp16") for _ in range(2)]
+    out = np.empty_like(x)
+    dsfft.execute_multi(plans, 0, x, out, batch)
+    single = np.empty_like(x)
+    dsfft.execute_host(plans[0], 0, x, single, batch)
+    assert out.tobytes() == single.tobytes()
+    want = to_work(_checker().forward(ref_inputs(orc, n, batch, 21, "fp16"), "dual", "fp16"),
+                   "fp16")
+    assert bit_mismatches(out, want) == 0
