@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsfft", choices=["dsfft", "reference"])
     ap.add_argument("--n", type=int, default=DEFAULT_N)
-    ap.add_argument("--batch", type=int, default=DEFAULT_BATCH, help="transforms per GPU")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="transforms per GPU (default 2^20 for N<=4096, else 1 GiB of input)")
     ap.add_argument("--precision", default="fp16", choices=["fp16", "fp32"])
     ap.add_argument("--strategy", default="dual")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -201,6 +202,9 @@ def accuracy_sample(y_host: np.ndarray, x_host: np.ndarray, n: int):
 
 def main():
     args = parse()
+    if args.batch is None:  # BASELINE configs[1] / configs[4]
+        sb = 4 if args.precision == "fp16" else 8
+        args.batch = DEFAULT_BATCH if args.n <= 4096 else max(1, (1 << 30) // (args.n * sb))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

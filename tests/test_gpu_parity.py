@@ -144,6 +144,49 @@ def test_errors(dsfft, cuda):
         dsfft.forward_f64(p64, np.zeros(64, dtype=np.complex128))
 
 
+LARGE = [2 ** m for m in range(13, 21)]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+@pytest.mark.parametrize("n", LARGE)
+@pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
+def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
+    """N = 2^13..2^20: 2-3 pass-group launches, L2-chunked batch."""
+    chk = _checker()
+    batch = 3 if n <= 1 << 16 else 2
+    strategies = ALL_STRATEGIES if n <= 1 << 14 else ("dual", "lf")
+    x = ref_inputs(orc, n, batch, seed=n + 7, precision=precision)
+    for s in strategies:
+        plan = dsfft.make_plan(n, s, precision)
+        y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+        want = to_work((chk.inverse if inverse else chk.forward)(x, s, precision), precision)
+        assert bit_mismatches(y, want) == 0, (n, s, precision)
+
+
+@pytest.mark.parametrize("m", [21, 22, 23, 24])
+def test_multipass_largest_sizes(dsfft, cuda, orc, m):
+    """Up to the reference's 2^24 cap (fft.cpp:14): one fp32 dual transform."""
+    chk = _checker()
+    n = 1 << m
+    x = ref_inputs(orc, n, 1, seed=m, precision="fp32")
+    plan = dsfft.make_plan(n, "dual", "fp32")
+    y = _device_run(dsfft, cuda, plan, to_work(x, "fp32"), False)
+    assert bit_mismatches(y, to_work(chk.forward(x, "dual", "fp32"), "fp32")) == 0
+
+
+def test_multipass_many_chunks(dsfft, cuda, orc):
+    """A batch spanning several L2 chunks (spot-checked transforms)."""
+    chk = _checker()
+    n = 1 << 16
+    batch = 400  # 256 KiB per fp16 transform -> several 48 MiB chunks
+    x = ref_inputs(orc, n, batch, seed=3, precision="fp16")
+    plan = dsfft.make_plan(n, "dual", "fp16")
+    y = _device_run(dsfft, cuda, plan, to_work(x, "fp16"), False)
+    idx = np.array([0, 1, 191, 192, 193, 250, batch - 1])
+    want = to_work(chk.forward(x[idx], "dual", "fp16"), "fp16")
+    assert bit_mismatches(y[idx], want) == 0
+
+
 def test_execute_multi_partitioner(dsfft, cuda, orc):
     """dsfft_execute_multi: contiguous shards on each listed device (here the
     one B200 twice, two host threads) reproduce the single-call result."""
