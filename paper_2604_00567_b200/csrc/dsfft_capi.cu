@@ -130,7 +130,7 @@ void choose_small_launch(dsfft_plan_s* p, int default_stages) {
   const dsfft::SmallGeom& g = p->small->geom;
   const int T = 32 * g.warps;
   int stages = env_int("DSFFT_STAGES", default_stages);
-  stages = std::max(2, std::min(stages, 8));
+  stages = std::max(1, std::min(stages, 8));
   int max_groups = std::max(1, g.max_threads / T);
   int want = env_int("DSFFT_GROUPS", 0);
   int groups = 0;
@@ -140,7 +140,7 @@ void choose_small_launch(dsfft_plan_s* p, int default_stages) {
       break;
     }
   }
-  while (groups == 0 && stages > 2) {  // shrink the ring if even one group does not fit
+  while (groups == 0 && stages > 1) {  // shrink the ring if even one group does not fit
     --stages;
     if (p->small->smem_bytes(1, stages) <= p->smem_optin) groups = 1;
   }

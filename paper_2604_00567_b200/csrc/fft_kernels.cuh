@@ -118,8 +118,8 @@ __device__ __forceinline__ void butterfly(uint32_t are, uint32_t aim, uint32_t b
       Bre = A::sub(are, t);
     } else {
       // record: ((-t, t), (w', w), sel_xy, sel_yx)
-      const uint32_t xy = __byte_perm(bre, bre, tw.z);
-      const uint32_t yx = __byte_perm(bre, bre, tw.w);
+      const uint32_t xy = ptx::prmt(bre, bre, tw.z);
+      const uint32_t yx = ptx::prmt(bre, bre, tw.w);
       const uint32_t u = A::fma(tw.x, yx, xy);
       Are = A::fma(u, tw.y, are);
       Bre = A::fma(u, A::neg(tw.y), are);
@@ -138,8 +138,8 @@ __device__ __forceinline__ void butterfly(uint32_t are, uint32_t aim, uint32_t b
     Bim = A::sub(aim, ti);
   } else {
     // record: (t, w', w, sel)
-    const uint32_t x = __byte_perm(bre, bim, tw.w);
-    const uint32_t y = __byte_perm(bim, bre, tw.w);
+    const uint32_t x = ptx::prmt(bre, bim, tw.w);
+    const uint32_t y = ptx::prmt(bim, bre, tw.w);
     const uint32_t u1 = A::fma(A::neg(tw.x), y, x);
     const uint32_t u2 = A::fma(tw.x, x, y);
     Are = A::fma(u1, tw.y, are);

@@ -17,10 +17,10 @@ using CfgW = Sched<DSFFT_M, 5, 1, DSFFT_M>;
 using CfgC = CfgW;
 #elif DSFFT_M == 6
 using CfgW = Sched<6, 5, 1, 3, 3>;
-using CfgC = CfgW;
+using CfgC = Sched<6, 5, 1, 1, 4, 1>;  // conflict-free for 4-byte values
 #elif DSFFT_M == 7
 using CfgW = Sched<7, 5, 1, 4, 3>;
-using CfgC = CfgW;
+using CfgC = Sched<7, 5, 1, 1, 5, 1>;
 #elif DSFFT_M == 8
 using CfgW = Sched<8, 5, 1, 4, 4>;
 using CfgC = CfgW;
@@ -31,10 +31,12 @@ using CfgC = CfgW;
 using CfgW = Sched<10, 5, 1, 5, 5>;
 using CfgC = CfgW;
 #elif DSFFT_M == 11
-using CfgW = Sched<11, 6, 1, 5, 6>;
+// 32 values per thread over 2 warps: (E=64, 1 warp) needed ~210 registers and
+// 33 KB per group, leaving ~4 resident warps per SM
+using CfgW = Sched<11, 5, 2, 5, 5, 1>;
 using CfgC = CfgW;
 #elif DSFFT_M == 12
-using CfgW = Sched<12, 6, 2, 6, 6>;
+using CfgW = Sched<12, 5, 4, 5, 5, 2>;
 using CfgC = CfgW;
 #else
 #error "single-kernel path covers N <= 4096"
@@ -47,12 +49,14 @@ SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   e.v[kVarF32] = make_variant<CfgW, ArithF32>();
   e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
   e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
-  // B200 sweeps at N=1024 (profiles/README.md): fp16 pairs S=2 x 12 groups
-  // 93% of HBM vs complex-per-register 83%; fp32 S=3 x 8 groups 96%.
-  e.f16_default = kVarF16P;
-  e.stages[kVarF32] = 3;
-  e.stages[kVarF16P] = 2;
-  e.stages[kVarF16C] = 2;
+  // Defaults from B200 sweeps (profiles/README.md, "launch shapes"):
+  // fp16 one-complex-per-register wins for N <= 512 (94% of HBM at 512),
+  // transform pairs for N >= 1024 (98% at 1024); N >= 2048 is shared-memory
+  // bound (twiddles ~N*16 B), where a 1-deep ring with more groups wins.
+  e.f16_default = DSFFT_M >= 10 ? kVarF16P : kVarF16C;
+  e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : 3;
+  e.stages[kVarF16P] = DSFFT_M >= 11 ? 1 : 2;
+  e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : 2;
   return e;
 }
 

@@ -8,18 +8,21 @@
 // (r + 2^P*rl') * N/2^(P+pl'+1), and scatters to q*2^(P+s) + r + 2^P*c'.
 //
 // CTA tile = 32 consecutive groups ("columns") x 2^s rows:
-//   * first group (P = 0): columns are 32 consecutive q; a column's outputs
-//     are 2^s contiguous samples;
-//   * later groups (P >= 5): columns are 32 consecutive r at fixed q, so
-//     every row of the tile is 32 contiguous samples in and out.
-// Inside the CTA: stage 1 = 5 passes in registers (lane = column, warp =
-// row group), exchange through padded smem, stage 2 = s-5 passes in
-// registers; lanes always walk contiguous samples, so each warp load/store
-// moves whole 128-byte lines.  Twiddle records are laid out per kernel in
-// exactly the order lanes consume them (coalesced 16-byte loads from L2).
+//   * first group (P = 0): columns are 32 consecutive q; each column's
+//     outputs are 2^s contiguous samples;
+//   * later groups (P >= 6): columns are 32 consecutive r at fixed q; every
+//     row of the tile is 32 contiguous samples in and out.
+// A persistent CTA owns a contiguous range of tiles (transform index fastest,
+// so consecutive tiles share their twiddles) and keeps S tiles in flight:
+// TMA tensor loads (3-D / 4-D maps with the batch as a coordinate, SASS
+// UTMALDG) land each tile row-major in a shared-memory ring slot.  Stage 1 =
+// 5 passes in registers (lane = column), exchange through the padded slot,
+// stage 2 = s-5 passes; the slot is handed back to TMA right after the last
+// smem read and results are stored straight from registers (full lines).
 //
-// The batch runs in chunks whose intermediate fits in L2 (126 MB), so the
-// pass groups after the first read their input from L2, not HBM.
+// The batch runs in chunks whose intermediate fits in L2, so pass groups
+// after the first read their input from L2 rather than HBM.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,92 +42,155 @@ thread_local std::string g_mp_err;
 const char* multipass_error() { return g_mp_err.c_str(); }
 
 struct MpParams {
-  const uint8_t* in;
-  uint8_t* out;
-  const uint4* tw;  // this pass group's records
-  int m, P;         // log2 N, first pass of the group
-  long long tiles_per_transform;
-  long long tiles;  // chunk transforms x tiles_per_transform
+  uint8_t* out;      // output of this pass group (chunk base)
+  const uint4* tw;   // this pass group's twiddle records (see mp_*_records)
+  int m, P;          // log2 N, first pass of the group
+  int stages;        // ring depth
+  long long nb;      // transforms in this chunk
+  long long b_off;   // first transform of the chunk (tensor-map coordinate)
+  long long tiles;   // nb * tiles_per_transform
   uint32_t scale;
-  int last;         // output is the user's buffer (stream it out of L2)
 };
 
-// Twiddle record offsets inside one pass group's table.
-//   stage 1 (local passes 0..4): slot (2^pl - 1 + rl) in 0..30
-//   stage 2 (local passes 5..s-1): slot 31 + (2^pl - 1 + rl) * 32 + r_l
-// and, for later groups, times 2^P + r (the column's global frequency).
-__host__ __device__ constexpr int mp_slot1(int pl, int rl) { return (1 << pl) - 1 + rl; }
-__host__ __device__ constexpr int mp_slot2(int pl, int rl, int r_l) {
-  return 31 + (((1 << pl) - 1 + rl) << 5) + r_l;
+// ---- twiddle table layouts (host and device agree) ---------------------------
+// first group (P = 0, twiddles independent of the column):
+//   [0, 31)                      stage 1, slot1 = 2^pl - 1 + rl
+//   31 + slot2*32 + r_l          stage 2, slot2 = 2^pl - 1 + rl, r_l < 32
+// later groups, per block of 32 columns (rb = r / 32), base rb * mp_block:
+//   slot1*32 + lane                          stage 1
+//   31*32 + (slot2*32 + r_l)*32 + lane       stage 2
+__host__ __device__ constexpr int mp_first_records(int S1) { return 31 + (((1 << S1) - 1) << 5); }
+__host__ __device__ constexpr int mp_block_records(int S1) {
+  return 31 * 32 + (((1 << S1) - 1) << 10);
 }
-__host__ __device__ constexpr int mp_slots(int s) { return 31 + (((1 << (s - 5)) - 1) << 5); }
 
-template <class A>
-__device__ __forceinline__ void mp_load(const uint8_t* base, long long idx, uint32_t& re,
-                                        uint32_t& im, bool streaming) {
-  if constexpr (A::kWords == 1) {
-    const unsigned int* p = reinterpret_cast<const unsigned int*>(base) + idx;
-    re = streaming ? __ldcs(p) : __ldcg(p);
-  } else {
-    const uint2* p = reinterpret_cast<const uint2*>(base) + idx;
-    const uint2 v = streaming ? __ldcs(p) : __ldcg(p);
-    re = v.x;
-    im = v.y;
+template <int S1, class A>
+struct MpLayout {
+  static constexpr int s = 5 + S1, L = 1 << s, T = 32 << S1;
+  static constexpr int VB = A::kWords * 4;
+  static constexpr int kBufBytes = 32 * (L + 1) * VB;  // padded exchange >= TMA tile
+  static constexpr int kTileBytes = 32 * L * VB;
+  // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned
+  __host__ __device__ static constexpr int tw_bytes(bool first) {
+    return ((first ? mp_first_records(S1) * 16 : 31 * 32 * 16) + 127) & ~127;
   }
-}
-
-template <class A>
-__device__ __forceinline__ void mp_store(uint8_t* base, long long idx, uint32_t re, uint32_t im,
-                                         bool streaming) {
-  if constexpr (A::kWords == 1) {
-    unsigned int* p = reinterpret_cast<unsigned int*>(base) + idx;
-    if (streaming) __stcs(p, re); else __stcg(p, re);
-  } else {
-    uint2* p = reinterpret_cast<uint2*>(base) + idx;
-    if (streaming) __stcs(p, make_uint2(re, im)); else __stcg(p, make_uint2(re, im));
+  static size_t smem_bytes(bool first, int stages) {
+    const int tw = tw_bytes(first);
+    return size_t(tw) + size_t(stages) * kBufBytes + size_t(stages) * 8;
   }
+};
+
+template <int S1, class A>
+constexpr int mp_min_blocks() {
+  // one-word values fit ~80 registers; two-word ~128
+  return 65536 / ((32 << S1) * (A::kWords == 1 ? 80 : 128)) > 0
+             ? 65536 / ((32 << S1) * (A::kWords == 1 ? 80 : 128))
+             : 1;
 }
 
-// One pass group over all tiles of a chunk.  T = 32 * 2^S1 threads; each
-// thread owns 32 values in stage 1 and 2^(5-S1) groups of 2^S1 in stage 2.
-template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT>
-__global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const MpParams p) {
-  constexpr int s = 5 + S1, L = 1 << s, T = 32 << S1, NG2 = 32 >> S1;
-  constexpr int VB = A::kWords * 4;                 // bytes per value
-  constexpr int STRIDE = L + 1;                     // padded smem column (values)
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t sbase = ptx::smem_u32(smem);
+template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST>
+__global__ void __launch_bounds__(32 << S1, mp_min_blocks<S1, A>())
+    mp_kernel(const __grid_constant__ CUtensorMap in_map, const MpParams p) {
+  using Lay = MpLayout<S1, A>;
+  constexpr int L = Lay::L, T = Lay::T, NG2 = 32 >> S1, VB = Lay::VB;
+  constexpr int STRIDE = L + 1;  // padded exchange column (values)
+  constexpr int ROWS_BOX = L < 256 ? L : 256;
+  extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long N = 1LL << p.m;
-  const long long rows_stride = N >> s;             // input row stride (samples)
+  const int S = p.stages;
   const int P = p.P;
+  const long long N = 1LL << p.m;
+  constexpr int tw_bytes = Lay::tw_bytes(FIRST);
+  uint4* tws = reinterpret_cast<uint4*>(smem);
+  const uint32_t tw_base = ptx::smem_u32(smem);
+  uint8_t* bufs = smem + tw_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(S) * Lay::kBufBytes);
+  const long long rblocks = FIRST ? 1 : ((1LL << P) >> 5);
 
-  for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-    const long long b = tile / p.tiles_per_transform;  // transform within chunk
-    const long long tt = tile - b * p.tiles_per_transform;
-    const uint8_t* gin = p.in + b * N * (A::kPair == 1 ? A::kSampleBytes : 4);
-    uint8_t* gout = p.out + b * N * (A::kPair == 1 ? A::kSampleBytes : 4);
-    // column (group) of this lane in stage 1 and its global frequency r
-    long long g;   // group index g = q*2^P + r
-    int r;         // 0 for the first group
-    if constexpr (FIRST) {
-      g = tt * 32 + lane;
-      r = 0;
-    } else {
-      const long long rblocks = (1LL << P) >> 5;
-      const long long q = tt / rblocks;
-      r = int((tt - q * rblocks) * 32 + lane);
-      g = (q << P) + r;
+  if constexpr (FIRST) {  // column-independent twiddles: stage once per CTA
+    for (int i = threadIdx.x; i < mp_first_records(S1); i += T) tws[i] = p.tw[i];
+  }
+  if (threadIdx.x == 0)
+    for (int b = 0; b < S; ++b) ptx::mbar_init(&bars[b], 1);
+  ptx::fence_mbar_init();
+  __syncthreads();
+
+  const long long per = (p.tiles + gridDim.x - 1) / gridDim.x;
+  const long long t_begin = blockIdx.x * per;
+  const long long t_end = t_begin + per < p.tiles ? t_begin + per : p.tiles;
+  const bool leader = threadIdx.x == 0;
+  uint64_t pol = 0;
+  if (leader) pol = ptx::policy_evict_first();
+  auto issue_load = [&](long long tile, int slot) {
+    const long long tt = tile / p.nb;
+    const int b = int(tile - tt * p.nb + p.b_off);
+    uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
+    ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
+#pragma unroll
+    for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
+      if constexpr (FIRST) {
+        ptx::tma_load_3d(dst + size_t(r0) * 32 * VB, &in_map, int(tt * 32), r0, b, &bars[slot],
+                         pol);
+      } else {
+        const long long q = tt / rblocks;
+        const int rb = int(tt - q * rblocks);
+        ptx::tma_load_4d(dst + size_t(r0) * 32 * VB, &in_map, rb * 32, int(q), r0, b,
+                         &bars[slot], pol);
+      }
     }
-    const long long g0 = g - lane;
+  };
+  if (leader)
+    for (int i = 0; i < S && t_begin + i < t_end; ++i) issue_load(t_begin + i, i);
+
+  long long staged_rb = -1;
+  // tile -> (tt, b) and tt -> (q, rb), advanced incrementally (no divisions)
+  const int nb = int(p.nb);
+  int b = int(t_begin % nb);
+  long long tt = t_begin / nb;
+  long long q = FIRST ? tt : tt / rblocks;
+  int rb = FIRST ? 0 : int(tt - q * rblocks);
+  int it = 0, it_slot = 0;
+  uint32_t it_phase = 0;
+  for (long long tile = t_begin; tile < t_end; ++tile, ++it) {
+    if (it > 0 && ++it_slot == S) {
+      it_slot = 0;
+      it_phase ^= 1;
+    }
+    if (it > 0 && ++b == nb) {
+      b = 0;
+      ++tt;
+      if constexpr (FIRST) {
+        q = tt;
+      } else if (++rb == rblocks) {
+        rb = 0;
+        ++q;
+      }
+    }
+    const int slot = it_slot;
+    if constexpr (!FIRST) {
+      if (rb != staged_rb) {  // new column block: stage its stage-1 twiddles
+        __syncthreads();
+        const uint4* src = p.tw + (long long)rb * mp_block_records(S1);
+        for (int i = threadIdx.x; i < 31 * 32; i += T) tws[i] = src[i];
+        __syncthreads();
+        staged_rb = rb;
+      }
+    }
+    uint8_t* bp = bufs + size_t(slot) * Lay::kBufBytes;
+    const uint32_t buf = ptx::smem_u32(bp);
+    ptx::mbar_wait(&bars[slot], it_phase);
+
     uint32_t re[32], im[32];
-    // ---- stage 1: rows warp + c*2^S1 of this lane's column ------------------
+    // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) ----
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const int row = warp + (c << S1);
-      mp_load<A>(gin, g + row * rows_stride, re[c], im[c], FIRST);
-      if constexpr (CONJ_IN) {  // conj on load (fft.cpp:90-91)
-        if constexpr (A::kWords == 1) re[c] ^= 0x80000000u; else im[c] = A::neg(im[c]);
+      const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
+      if constexpr (A::kWords == 1) {
+        re[c] = ptx::lds32(a);
+        if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
+      } else {
+        ptx::lds64(a, re[c], im[c]);
+        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
       }
     }
 #pragma unroll
@@ -132,13 +198,13 @@ __global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const Mp
       uint32_t nre[32], nim[32];
 #pragma unroll
       for (int rl = 0; rl < (1 << pl); ++rl) {
-        const long long idx = FIRST ? mp_slot1(pl, rl)
-                                    : ((long long)mp_slot1(pl, rl) << P) + r;
-        const uint4 tw = __ldg(p.tw + idx);
+        const int slot1 = (1 << pl) - 1 + rl;
+        const uint4 tw = FIRST ? ptx::lds128(tw_base + slot1 * 16)
+                               : ptx::lds128(tw_base + (slot1 * 32 + lane) * 16);
 #pragma unroll
-        for (int q = 0; q < (16 >> pl); ++q) {
-          const int jl = (q << pl) | rl;
-          const int oa = (q << (pl + 1)) + rl;
+        for (int qq = 0; qq < (16 >> pl); ++qq) {
+          const int jl = (qq << pl) | rl;
+          const int oa = (qq << (pl + 1)) + rl;
           butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa], nim[oa],
                                  nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
         }
@@ -149,33 +215,35 @@ __global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const Mp
         if constexpr (A::kWords == 2) im[i] = nim[i];
       }
     }
-    // ---- exchange: local position warp*32 + c' of column lane ----------------
-    __syncthreads();  // previous tile's stage-2 reads are done
+    // ---- exchange through the padded slot: [col][local pos] -----------------
+    __syncthreads();  // every stage-1 read of the TMA tile is done
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const uint32_t a = sbase + (lane * STRIDE + warp * 32 + c) * VB;
+      const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
       if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
     }
     __syncthreads();
-    // ---- stage 2: groups (column, r_l), values at local rows r_l + 32*c ------
-    int col[NG2], rloc[NG2];
+    // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
+    // column output), later groups lanes walk columns (contiguous rows)
 #pragma unroll
     for (int j = 0; j < NG2; ++j) {
-      const int glin = threadIdx.x + T * j;
-      if constexpr (FIRST) {  // lanes walk r_l: contiguous column output
-        rloc[j] = glin & 31;
-        col[j] = glin >> 5;
-      } else {                // lanes walk columns: contiguous row output
-        col[j] = glin & 31;
-        rloc[j] = glin >> 5;
-      }
+      const int col = FIRST ? warp + (j << S1) : lane;
+      const int rl_ = FIRST ? lane : warp + (j << S1);
 #pragma unroll
       for (int c = 0; c < (1 << S1); ++c) {
-        const uint32_t a = sbase + (col[j] * STRIDE + rloc[j] + 32 * c) * VB;
+        const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
         const int v = (j << S1) + c;
         if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
       }
     }
+    // release the slot to the tile S ahead
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (leader && tile + S < t_end) issue_load(tile + S, slot);
+    // ---- stage 2 ------------------------------------------------------------
+    const uint4* tw2 = FIRST ? nullptr
+                             : p.tw + (long long)rb * mp_block_records(S1) + 31 * 32 +
+                                   warp * 32 + lane;
 #pragma unroll
     for (int pl = 0; pl < S1; ++pl) {
       uint32_t nre[32], nim[32];
@@ -183,15 +251,17 @@ __global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const Mp
       for (int rl = 0; rl < (1 << pl); ++rl)
 #pragma unroll
         for (int j = 0; j < NG2; ++j) {
-          const int rcol = FIRST ? 0 : r - lane + col[j];  // global r of this group's column
-          const long long idx = FIRST ? mp_slot2(pl, rl, rloc[j])
-                                      : ((long long)mp_slot2(pl, rl, rloc[j]) << P) + rcol;
-          const uint4 tw = __ldg(p.tw + idx);
+          const int slot2 = (1 << pl) - 1 + rl;
+          uint4 tw;
+          if constexpr (FIRST)
+            tw = ptx::lds128(tw_base + (31 + (slot2 << 5) + lane) * 16);
+          else  // record (slot2*32 + r_l)*32 + lane, r_l = warp + 2^S1 j
+            tw = __ldg(tw2 + ((slot2 << 5) + (j << S1)) * 32);
 #pragma unroll
-          for (int q = 0; q < ((1 << (S1 - 1)) >> pl); ++q) {
-            const int jl = (q << pl) | rl;
+          for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
+            const int jl = (qq << pl) | rl;
             const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
-            const int oa = (j << S1) + (q << (pl + 1)) + rl;
+            const int oa = (j << S1) + (qq << (pl + 1)) + rl;
             butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
                                    nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
           }
@@ -202,7 +272,17 @@ __global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const Mp
         if constexpr (A::kWords == 2) im[i] = nim[i];
       }
     }
-    // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') ------------------------
+    // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') --------------------------
+    uint8_t* gout = p.out + b * N * VB;
+    uint8_t* base;
+    long long cstride;  // bytes between output rows c'
+    if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c') VB
+      base = gout + ((q * 32 + warp) * L + lane) * VB;
+      cstride = 32 * VB;
+    } else {
+      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * VB;
+      cstride = ((long long)VB << P) * 32;
+    }
 #pragma unroll
     for (int j = 0; j < NG2; ++j)
 #pragma unroll
@@ -217,21 +297,28 @@ __global__ void __launch_bounds__(32 << S1, (512 >> S1) / 32) mp_kernel(const Mp
             xi = A::mul(A::neg(xi), p.scale);
           }
         }
-        const int lrow = rloc[j] + 32 * c;  // local output row c'
-        long long pos;
-        if constexpr (FIRST) {
-          pos = (g0 + col[j]) * L + lrow;  // column-contiguous (P = 0)
+        uint8_t* dst;
+        if constexpr (FIRST)
+          dst = base + ((long long)(j << S1) * L) * VB + c * cstride;
+        else
+          dst = base + (((long long)(j << S1) * VB) << P) + c * cstride;
+        if constexpr (A::kWords == 1) {
+          if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
+          else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
         } else {
-          const long long gc = g0 + col[j];
-          const long long q = gc >> P, rr = gc & ((1LL << P) - 1);
-          pos = (q << (P + s)) + rr + ((long long)lrow << P);
+          if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+          else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
         }
-        mp_store<A>(gout, pos, xr, xi, p.last != 0);
       }
   }
 }
 
 // ---- host side ---------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 struct MpGroup {
   int P, s;
@@ -240,6 +327,7 @@ struct MpGroup {
 
 struct MultipassPlan {
   int m = 0, strategy = 0, precision = 0, sm_count = 0;
+  size_t smem_optin = 0;
   std::vector<MpGroup> groups;
   uint8_t* scratch[2] = {nullptr, nullptr};
   size_t chunk_transforms = 0;
@@ -253,9 +341,24 @@ struct MultipassPlan {
 
 namespace {
 
-std::vector<int> split_passes(int m) {
-  // 2 groups up to m = 18, 3 beyond; every group 6..9 passes, first >= 5
-  if (m <= 18) {
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeFn(nullptr);
+    return reinterpret_cast<EncodeFn>(f);
+  }();
+  return fn;
+}
+
+std::vector<int> split_passes(int m, int max_s) {
+  // 2 groups up to m = 2*max_s, 3 beyond; every group 6..max_s passes
+  // (max_s = 9 for one-word fp16 values, 8 for fp32: a 2-deep ring of
+  // 32 x 2^s x 8-byte tiles must fit in shared memory)
+  if (m <= 2 * max_s) {
     const int a = (m + 1) / 2;
     return {a, m - a};
   }
@@ -263,77 +366,135 @@ std::vector<int> split_passes(int m) {
   return {a, b, m - a - b};
 }
 
+size_t sample_bytes(int precision) { return precision == kFp16 ? 4 : 8; }
+
+// Input map of a pass group over `batch` transforms starting at `base`.
+bool make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
+                 long long batch) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  const CUtensorMapDataType dt =
+      vb == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  const cuuint64_t N = cuuint64_t(1) << m;
+  const cuuint32_t rows_box = cuuint32_t(std::min(1 << s, 256));
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r;
+  if (P == 0) {  // {q (N/2^s), c (2^s), b}
+    cuuint64_t dims[3] = {N >> s, cuuint64_t(1) << s, cuuint64_t(batch)};
+    cuuint64_t strides[2] = {(N >> s) * vb, N * vb};
+    cuuint32_t box[3] = {32, rows_box, 1};
+    r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {  // {r (2^P), q (N/2^(P+s)), c (2^s), b}
+    cuuint64_t dims[4] = {cuuint64_t(1) << P, N >> (P + s), cuuint64_t(1) << s,
+                          cuuint64_t(batch)};
+    cuuint64_t strides[3] = {(cuuint64_t(1) << P) * vb, (N >> s) * vb, N * vb};
+    cuuint32_t box[4] = {32, 1, rows_box, 1};
+    r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
 template <int S1, class A, bool STD>
-cudaError_t mp_launch_t(const MpParams& p, bool first, bool conj_in, bool scale_out, int grid,
+cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, bool conj_in,
+                        bool scale_out, bool last, int sm_count, size_t smem_optin,
                         cudaStream_t st) {
-  constexpr int s = 5 + S1;
-  const size_t smem = size_t(32) * ((1 << s) + 1) * A::kWords * 4;
+  using Lay = MpLayout<S1, A>;
+  MpParams q = p;
+  int stages = 3;  // fp32 at s = 9 only fits a 1-deep ring (no prefetch, still correct)
+  while (stages > 1 && Lay::smem_bytes(first, stages) > smem_optin) --stages;
+  q.stages = stages;
+  const size_t smem = Lay::smem_bytes(first, stages);
+  const int per_sm = std::max(1, int(std::min<size_t>(smem_optin / smem, 2048 / Lay::T)));
+  const int grid = int(std::min<long long>(p.tiles, (long long)sm_count * per_sm));
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<grid, 32 << S1, smem, st>>>(p);
+    kern<<<grid, Lay::T, smem, st>>>(map, q);
     return cudaGetLastError();
   };
-  if (first)
-    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false>)
-                   : go(mp_kernel<S1, A, STD, true, false, false>);
-  return scale_out ? go(mp_kernel<S1, A, STD, false, false, true>)
-                   : go(mp_kernel<S1, A, STD, false, false, false>);
+  if (first)  // never last: every split has >= 2 groups
+    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false>)
+                   : go(mp_kernel<S1, A, STD, true, false, false, false>);
+  if (last)
+    return scale_out ? go(mp_kernel<S1, A, STD, false, false, true, true>)
+                     : go(mp_kernel<S1, A, STD, false, false, false, true>);
+  return go(mp_kernel<S1, A, STD, false, false, false, false>);
 }
 
 template <class A, bool STD>
-cudaError_t mp_launch_a(int S1, const MpParams& p, bool first, bool conj_in, bool scale_out,
-                        int grid, cudaStream_t st) {
+cudaError_t mp_launch_a(int S1, const CUtensorMap& map, const MpParams& p, bool first,
+                        bool conj_in, bool scale_out, bool last, int sm_count, size_t optin,
+                        cudaStream_t st) {
   switch (S1) {
-    case 1: return mp_launch_t<1, A, STD>(p, first, conj_in, scale_out, grid, st);
-    case 2: return mp_launch_t<2, A, STD>(p, first, conj_in, scale_out, grid, st);
-    case 3: return mp_launch_t<3, A, STD>(p, first, conj_in, scale_out, grid, st);
-    case 4: return mp_launch_t<4, A, STD>(p, first, conj_in, scale_out, grid, st);
+    case 1: return mp_launch_t<1, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
+    case 2: return mp_launch_t<2, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
+    case 3: return mp_launch_t<3, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
+    case 4: return mp_launch_t<4, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
   }
   return cudaErrorInvalidValue;
 }
 
-size_t sample_bytes(int precision) { return precision == kFp16 ? 4 : 8; }
-
 }  // namespace
 
 MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int strategy,
-                                int precision, int sm_count, size_t /*smem_optin*/) {
+                                int precision, int sm_count, size_t smem_optin) {
+  if (!encode_fn()) {
+    g_mp_err = "multipass: cuTensorMapEncodeTiled unavailable";
+    return nullptr;
+  }
   auto* mp = new MultipassPlan();
   mp->m = m;
   mp->strategy = strategy;
   mp->precision = precision;
   mp->sm_count = sm_count;
+  mp->smem_optin = smem_optin;
   const bool f16c = precision == kFp16;  // one complex per f16x2 register
+  auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
   int P = 0;
-  for (int s : split_passes(m)) {
+  for (int s : split_passes(m, 9)) {
     MpGroup g;
     g.P = P;
     g.s = s;
     const int S1 = s - 5;
-    const long long reps = P == 0 ? 1 : (1LL << P);
-    std::vector<Record> rec(size_t(mp_slots(s)) * reps);
-    for (long long r = 0; r < reps; ++r) {
-      // stage 1: local passes pl < 5, local freq rl' = rl
+    std::vector<Record> recs;
+    if (P == 0) {
+      recs.resize(mp_first_records(S1));
       for (int pl = 0; pl < 5; ++pl)
-        for (int rl = 0; rl < (1 << pl); ++rl) {
-          const long long k = (r + ((long long)rl << P)) << (m - P - pl - 1);
-          rec[size_t(mp_slot1(pl, rl)) * reps + r] =
-              pack_record(table[k], strategy, precision, f16c);
-        }
-      // stage 2: local passes 5 + pl, local freq rl' = r_l + 32 rl
+        for (int rl = 0; rl < (1 << pl); ++rl)
+          recs[(1 << pl) - 1 + rl] = rec((long long)rl << (m - pl - 1));
       for (int pl = 0; pl < S1; ++pl)
         for (int rl = 0; rl < (1 << pl); ++rl)
-          for (int r_l = 0; r_l < 32; ++r_l) {
-            const long long lf = r_l + 32LL * rl;
-            const long long k = (r + (lf << P)) << (m - P - 5 - pl - 1);
-            rec[size_t(mp_slot2(pl, rl, r_l)) * reps + r] =
-                pack_record(table[k], strategy, precision, f16c);
-          }
+          for (int r_l = 0; r_l < 32; ++r_l)
+            recs[31 + (((1 << pl) - 1 + rl) << 5) + r_l] =
+                rec((r_l + 32LL * rl) << (m - 5 - pl - 1));
+    } else {
+      const long long blocks = (1LL << P) >> 5;
+      const int per = mp_block_records(S1);
+      recs.resize(size_t(blocks) * per);
+      for (long long rb = 0; rb < blocks; ++rb)
+        for (int lane = 0; lane < 32; ++lane) {
+          const long long r = rb * 32 + lane;
+          Record* blk = recs.data() + rb * per;
+          for (int pl = 0; pl < 5; ++pl)
+            for (int rl = 0; rl < (1 << pl); ++rl)
+              blk[((1 << pl) - 1 + rl) * 32 + lane] =
+                  rec((r + ((long long)rl << P)) << (m - P - pl - 1));
+          for (int pl = 0; pl < S1; ++pl)
+            for (int rl = 0; rl < (1 << pl); ++rl)
+              for (int r_l = 0; r_l < 32; ++r_l) {
+                const long long lf = r_l + 32LL * rl;  // local frequency
+                blk[31 * 32 + ((((1 << pl) - 1 + rl) << 5) + r_l) * 32 + lane] =
+                    rec((r + (lf << P)) << (m - P - 5 - pl - 1));
+              }
+        }
     }
-    if (cudaMalloc(&g.d_tw, rec.size() * sizeof(Record)) != cudaSuccess ||
-        cudaMemcpy(g.d_tw, rec.data(), rec.size() * sizeof(Record), cudaMemcpyHostToDevice) !=
+    if (cudaMalloc(&g.d_tw, recs.size() * sizeof(Record)) != cudaSuccess ||
+        cudaMemcpy(g.d_tw, recs.data(), recs.size() * sizeof(Record), cudaMemcpyHostToDevice) !=
             cudaSuccess) {
       g_mp_err = "multipass: twiddle upload failed";
       mp->groups.push_back(g);
@@ -361,37 +522,50 @@ void multipass_destroy(MultipassPlan* mp) { delete mp; }
 
 int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, size_t batch,
                       uint32_t scale, cudaStream_t stream, uint64_t* launches) {
-  const size_t tb = (size_t(1) << mp.m) * sample_bytes(mp.precision);
+  const int vb = int(sample_bytes(mp.precision));
+  const size_t tb = (size_t(1) << mp.m) * vb;
   const bool f16 = mp.precision == kFp16;
   const bool std_ = mp.strategy == kStandard;
   const int ng = int(mp.groups.size());
+  // maps: the user input over the whole batch (chunk = coordinate offset) and
+  // the two fixed scratch buffers
+  std::vector<CUtensorMap> maps(ng);
+  for (int i = 0; i < ng; ++i) {
+    const void* base = i == 0 ? in : mp.scratch[(i - 1) & 1];
+    const long long nb = i == 0 ? (long long)batch : (long long)mp.chunk_transforms;
+    if (!make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s, vb, nb)) {
+      g_mp_err = "multipass: cuTensorMapEncodeTiled failed";
+      return 1;
+    }
+  }
   for (size_t b0 = 0; b0 < batch; b0 += mp.chunk_transforms) {
     const size_t nb = std::min(mp.chunk_transforms, batch - b0);
     for (int i = 0; i < ng; ++i) {
       const MpGroup& g = mp.groups[i];
       MpParams p{};
-      p.in = i == 0 ? static_cast<const uint8_t*>(in) + b0 * tb : mp.scratch[(i - 1) & 1];
       p.out = i == ng - 1 ? static_cast<uint8_t*>(out) + b0 * tb : mp.scratch[i & 1];
       p.tw = g.d_tw;
       p.m = mp.m;
       p.P = g.P;
-      p.tiles_per_transform = ((1LL << mp.m) >> g.s) / 32;
-      p.tiles = p.tiles_per_transform * (long long)nb;
+      p.nb = (long long)nb;
+      p.b_off = i == 0 ? (long long)b0 : 0;
+      p.tiles = (((1LL << mp.m) >> g.s) / 32) * (long long)nb;
       p.scale = scale;
-      p.last = i == ng - 1;
-      const int threads = 32 << (g.s - 5);
-      const int per_sm = std::max(1, 2048 / threads);
-      const int grid = int(std::min<long long>(p.tiles, (long long)mp.sm_count * per_sm));
       const bool first = i == 0, last = i == ng - 1;
+      const int S1 = g.s - 5;
       cudaError_t e =
-          f16 ? (std_ ? mp_launch_a<ArithF16C, true>(g.s - 5, p, first, first && inverse,
-                                                     last && inverse, grid, stream)
-                      : mp_launch_a<ArithF16C, false>(g.s - 5, p, first, first && inverse,
-                                                      last && inverse, grid, stream))
-              : (std_ ? mp_launch_a<ArithF32, true>(g.s - 5, p, first, first && inverse,
-                                                    last && inverse, grid, stream)
-                      : mp_launch_a<ArithF32, false>(g.s - 5, p, first, first && inverse,
-                                                     last && inverse, grid, stream));
+          f16 ? (std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, first && inverse,
+                                                     last && inverse, last, mp.sm_count,
+                                                     mp.smem_optin, stream)
+                      : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, first && inverse,
+                                                      last && inverse, last, mp.sm_count,
+                                                      mp.smem_optin, stream))
+              : (std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, first && inverse,
+                                                    last && inverse, last, mp.sm_count,
+                                                    mp.smem_optin, stream)
+                      : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, first && inverse,
+                                                     last && inverse, last, mp.sm_count,
+                                                     mp.smem_optin, stream));
       if (e != cudaSuccess) {
         g_mp_err = std::string("mp_kernel launch: ") + cudaGetErrorString(e);
         return 1;

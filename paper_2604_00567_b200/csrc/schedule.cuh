@@ -94,7 +94,9 @@ struct Sched {
   }
   // Twiddle table offsets (in 16-byte records) of each stage.
   DSFFT_HD static constexpr int tw_off(int i) {
-    return i == 0 ? 0 : tw_off(i - 1) + tw_stage_size(P(i - 1), s(i - 1));
+    int off = 0;
+    for (int k = 0; k < i; ++k) off += tw_stage_size(P(k), s(k));
+    return off;
   }
   static constexpr int TW_RECORDS = tw_off(NSTAGE);
   static constexpr int BUF_VALS = padded_size(VALS);  // 8-byte values

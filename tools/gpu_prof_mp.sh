@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+C1="python bench.py --n 65536 --batch 192 --steps 1 --warmup 3 --no-cpu --no-e2e"
+C2="python bench.py --n 1048576 --batch 12 --steps 1 --warmup 3 --no-cpu --no-e2e"
+$C1 > gpurun_out/mp_plain1.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:mp_kernel -s 6 -c 2 -o gpurun_out/prof_mp65536 $C1 > gpurun_out/ncu_mp1.log 2>&1; echo rc1=$?
+$C2 > gpurun_out/mp_plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:mp_kernel -s 9 -c 3 -o gpurun_out/prof_mp1m $C2 > gpurun_out/ncu_mp2.log 2>&1; echo rc2=$?

@@ -28,7 +28,7 @@ using namespace dsfft;
 struct Cfg {
   int m, logE, W;
   std::vector<int> s;
-  int fp16;  // 1: values are packed transform pairs, identity layout is 4-byte half2
+  int fp16;  // 0 fp32; 1 fp16 transform pairs (identity 2 x half2); 2 fp16 complex (4-byte values)
 };
 
 // Wavefronts for one warp access: addr[lane] byte address, B bytes per lane.
@@ -123,6 +123,7 @@ static bool check(const Cfg& c, bool verbose) {
 
   // --- 2. bank conflicts (per warp 0..W-1, every access) -----------------
   Tally ld, ex_w, ex_r, stv, tw;
+  const int VB = c.fp16 == 2 ? 4 : 8;  // exchange value bytes
   P = 0;
   const int nst = int(c.s.size());
   for (int st = 0; st < nst; ++st) {
@@ -134,30 +135,31 @@ static bool check(const Cfg& c, bool verbose) {
           for (int l = 0; l < 32; ++l) {
             const int G = 32 * w + l + T * j;
             const int rp = read_pos(m, P, s, G, cc), wp = write_pos(m, P, s, G, cc);
-            if (c.fp16) {
+            if (c.fp16 == 1) {
               // identity: real transform 2k+h, half2 (4 bytes)
               ar[l] = long((2 * (rp / N)) * N + rp % N) * 4;
               ar1[l] = long((2 * (rp / N) + 1) * N + rp % N) * 4;
               aw[l] = long((2 * (wp / N)) * N + wp % N) * 4;
               aw1[l] = long((2 * (wp / N) + 1) * N + wp % N) * 4;
             } else {
-              ar[l] = long(rp) * 8;
-              aw[l] = long(wp) * 8;
+              ar[l] = long(rp) * VB;
+              aw[l] = long(wp) * VB;
             }
           }
-          if (st == 0) { ld.add(ar, c.fp16 ? 4 : 8); if (c.fp16) ld.add(ar1, 4); }
+          const int IB = c.fp16 ? 4 : 8;  // identity access width
+          if (st == 0) { ld.add(ar, IB); if (c.fp16 == 1) ld.add(ar1, 4); }
           else {
             std::vector<long> a(32);
             for (int l = 0; l < 32; ++l)
-              a[l] = long(pad_pos(read_pos(m, P, s, 32 * w + l + T * j, cc))) * 8;
-            ex_r.add(a, 8);
+              a[l] = long(pad_pos(read_pos(m, P, s, 32 * w + l + T * j, cc))) * VB;
+            ex_r.add(a, VB);
           }
-          if (st == nst - 1) { stv.add(aw, c.fp16 ? 4 : 8); if (c.fp16) stv.add(aw1, 4); }
+          if (st == nst - 1) { stv.add(aw, IB); if (c.fp16 == 1) stv.add(aw1, 4); }
           else {
             std::vector<long> a(32);
             for (int l = 0; l < 32; ++l)
-              a[l] = long(pad_pos(write_pos(m, P, s, 32 * w + l + T * j, cc))) * 8;
-            ex_w.add(a, 8);
+              a[l] = long(pad_pos(write_pos(m, P, s, 32 * w + l + T * j, cc))) * VB;
+            ex_w.add(a, VB);
           }
         }
         // twiddles: one LDS.128 per (pl, rl)
@@ -172,7 +174,7 @@ static bool check(const Cfg& c, bool verbose) {
     }
     P += s;
   }
-  printf("m=%2d logE=%d W=%d fp%d stages=", m, c.logE, c.W, c.fp16 ? 16 : 32);
+  printf("m=%2d logE=%d W=%d %s stages=", m, c.logE, c.W, c.fp16 == 2 ? "f16c" : c.fp16 ? "f16p" : "fp32");
   for (int s : c.s) printf("%d ", s);
   printf("| dataflow %s | wavefronts actual/ideal: load %ld/%ld exw %ld/%ld exr %ld/%ld "
          "store %ld/%ld tw %ld/%ld\n",
@@ -188,6 +190,8 @@ int main(int argc, char** argv) {
     c.fp16 = 0;
     bool ok = check(c, true);
     c.fp16 = 1;
+    ok = check(c, true) && ok;
+    c.fp16 = 2;
     ok = check(c, true) && ok;
     return ok ? 0 : 1;
   }
@@ -214,7 +218,7 @@ int main(int argc, char** argv) {
               comps.push_back(v);
             }
         for (auto& v : comps)
-          for (int f = 0; f <= 1; ++f) {
+          for (int f = 0; f <= 2; ++f) {
             Cfg c{m, logE, W, v, f};
             if (!check(c, false)) ++bad;
           }
