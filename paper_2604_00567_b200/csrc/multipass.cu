@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -71,8 +72,13 @@ struct MpLayout {
   static constexpr int kBufBytes = 32 * (L + 1) * VB;  // padded exchange >= TMA tile
   static constexpr int kTileBytes = 32 * L * VB;
   // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned
+  // later groups keep their column block's whole twiddle slab in smem (stage 1
+  // and 2) when it fits next to the ring (S1 <= 3: <= 130 KB); S1 = 4 stages
+  // only the stage-1 part and reads stage 2 through L1
+  static constexpr bool kFullSlab = S1 <= 3;
+  static constexpr int kSlabRecords = kFullSlab ? mp_block_records(S1) : 31 * 32;
   __host__ __device__ static constexpr int tw_bytes(bool first) {
-    return ((first ? mp_first_records(S1) * 16 : 31 * 32 * 16) + 127) & ~127;
+    return ((first ? mp_first_records(S1) * 16 : kSlabRecords * 16) + 127) & ~127;
   }
   static size_t smem_bytes(bool first, int stages) {
     const int tw = tw_bytes(first);
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(32 << S1, mp_min_blocks<S1, A>())
       if (rb != staged_rb) {  // new column block: stage its stage-1 twiddles
         __syncthreads();
         const uint4* src = p.tw + (long long)rb * mp_block_records(S1);
-        for (int i = threadIdx.x; i < 31 * 32; i += T) tws[i] = src[i];
+        for (int i = threadIdx.x; i < Lay::kSlabRecords; i += T) tws[i] = src[i];
         __syncthreads();
         staged_rb = rb;
       }
@@ -255,7 +261,10 @@ __global__ void __launch_bounds__(32 << S1, mp_min_blocks<S1, A>())
           uint4 tw;
           if constexpr (FIRST)
             tw = ptx::lds128(tw_base + (31 + (slot2 << 5) + lane) * 16);
-          else  // record (slot2*32 + r_l)*32 + lane, r_l = warp + 2^S1 j
+          else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
+            tw = ptx::lds128(tw_base + (31 * 32 + (warp << 5) + lane +
+                                        (((slot2 << 5) + (j << S1)) << 5)) * 16);
+          else  // r_l = warp + 2^S1 j
             tw = __ldg(tw2 + ((slot2 << 5) + (j << S1)) * 32);
 #pragma unroll
           for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
@@ -404,7 +413,9 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
                         cudaStream_t st) {
   using Lay = MpLayout<S1, A>;
   MpParams q = p;
-  int stages = 3;  // fp32 at s = 9 only fits a 1-deep ring (no prefetch, still correct)
+  // ring depth; fp32 at s = 9 only fits a 1-deep ring (no prefetch, still correct)
+  const char* env = std::getenv("DSFFT_MP_STAGES");
+  int stages = env && *env ? std::max(1, std::atoi(env)) : 2;
   while (stages > 1 && Lay::smem_bytes(first, stages) > smem_optin) --stages;
   q.stages = stages;
   const size_t smem = Lay::smem_bytes(first, stages);
@@ -506,7 +517,10 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   }
   // chunk so the intermediate (one scratch buffer) stays L2-resident
   const size_t tb = (size_t(1) << m) * sample_bytes(precision);
-  const size_t want = size_t(48) << 20;
+  const char* env = std::getenv("DSFFT_MP_CHUNK_MB");
+  // measured on B200 (profiles/README.md): L2-sized 48 MiB chunks lose more to
+  // per-launch ramp/tail than they gain from L2 residency; 1 GiB chunks win
+  const size_t want = size_t(env && *env ? std::atoi(env) : 1024) << 20;
   mp->chunk_transforms = std::max<size_t>(1, want / tb);
   const size_t bytes = mp->chunk_transforms * tb;
   for (auto*& s : mp->scratch)
