@@ -175,8 +175,10 @@ def sample_bytes(precision: str) -> int:
 
 def _torch_view(x, plan: FftPlan):
     import torch
-    want_c = torch.complex32 if plan.precision == "fp16" else torch.complex64
-    want_r = torch.float16 if plan.precision == "fp16" else torch.float32
+    want_c = {"fp16": torch.complex32, "fp32": torch.complex64,
+              "fp64": torch.complex128}[plan.precision]
+    want_r = {"fp16": torch.float16, "fp32": torch.float32,
+              "fp64": torch.float64}[plan.precision]
     if x.dtype == want_c:
         n = x.shape[-1]
     elif x.dtype == want_r and x.shape[-1] == 2:

@@ -14,6 +14,7 @@
 
 #include "../../include/dsfft.h"
 #include "host_table.hpp"
+#include "fp64.cuh"
 #include "multipass.cuh"
 #include "small_launch.cuh"
 
@@ -102,6 +103,8 @@ struct dsfft_plan_s {
   int groups = 0, stages = 0, grid = 0;
   // multi-pass path (m > 12)
   dsfft::MultipassPlan* mp = nullptr;
+  // fp64 path (per-pass DFMA kernels)
+  dsfft::F64Plan* f64 = nullptr;
   int sm_count = 0;
   size_t smem_optin = 0;
   std::mutex mu;
@@ -111,7 +114,9 @@ struct dsfft_plan_s {
 
 namespace {
 
-size_t sample_bytes(int p) { return p == DSFFT_FP16 ? 4 : p == DSFFT_FP32 ? 8 : 0; }
+size_t sample_bytes(int p) {
+  return p == DSFFT_FP16 ? 4 : p == DSFFT_FP32 ? 8 : p == DSFFT_FP64 ? 16 : 0;
+}
 
 uint32_t inverse_scale_word(const dsfft_plan_s* p) {
   const double s = dsfft::round_to(1.0 / double(p->n), p->precision);  // fft.cpp:92-93
@@ -175,6 +180,12 @@ int upload_small_tables(dsfft_plan_s* p) {
 int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
            cudaStream_t stream) {
   if (batch == 0) return DSFFT_OK;
+  if (p->f64) {
+    const int e = dsfft::fp64_execute(*p->f64, dir == DSFFT_INVERSE, in, out, batch,
+                                      1.0 / double(p->n), p->sm_count, stream, &g_launches);
+    if (e) return fail(DSFFT_ERR_CUDA, dsfft::fp64_error());
+    return DSFFT_OK;
+  }
   const uint32_t scale = inverse_scale_word(p);
   if (p->mp) {
     const int e = dsfft::multipass_execute(*p->mp, dir == DSFFT_INVERSE, in, out, batch, scale,
@@ -238,8 +249,6 @@ int check_exec_args(dsfft_plan_s* p, int dir, const void* in, void* out) {
   if (!p) return fail(DSFFT_ERR_INVALID, "null plan");
   if (dir != DSFFT_FORWARD && dir != DSFFT_INVERSE)
     return fail(DSFFT_ERR_INVALID, "unknown direction");
-  if (p->precision == DSFFT_FP64)
-    return fail(DSFFT_ERR_UNSUPPORTED, "fp64 execution is not on the device path");
   if (!in || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
   return DSFFT_OK;
 }
@@ -278,10 +287,6 @@ int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, i
   p->precision = precision;
   p->clamp_eps = clamp_eps;
   p->device = device;
-  if (precision == DSFFT_FP64) {  // table-only plan (introspection); execute refuses
-    *out = p;
-    return DSFFT_OK;
-  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     delete p;
@@ -301,7 +306,10 @@ int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, i
   p->smem_optin = prop.sharedMemPerBlockOptin;
   DeviceGuard guard(device);
   int rc = DSFFT_OK;
-  if (p->m <= 12) {
+  if (precision == DSFFT_FP64) {
+    p->f64 = dsfft::fp64_create(p->table, int(p->m), strategy);
+    if (!p->f64) rc = fail(DSFFT_ERR_CUDA, dsfft::fp64_error());
+  } else if (p->m <= 12) {
     const dsfft::SmallEntry& se = small_entry(int(p->m));
     p->variant = dsfft::kVarF32;
     if (precision == DSFFT_FP16) {
@@ -332,6 +340,7 @@ int dsfft_plan_destroy(dsfft_plan p) {
     if (p->scratch) cudaFree(p->scratch);
     delete p->pipe;
     if (p->mp) dsfft::multipass_destroy(p->mp);
+    if (p->f64) dsfft::fp64_destroy(p->f64);
   }
   delete p;
   return DSFFT_OK;
@@ -511,7 +520,7 @@ int dsfft_execute_f64(dsfft_plan p, int dir, const double* in, double* out, size
   int rc = check_exec_args(p, dir, in, out);
   if (rc) return rc;
   const size_t count = 2 * p->n * batch;
-  std::vector<uint8_t> a(count * (p->precision == DSFFT_FP16 ? 2 : 4) + 16);
+  std::vector<uint8_t> a(count * (sample_bytes(p->precision) / 2) + 16);
   std::vector<uint8_t> b(a.size());
   // 16-byte alignment is not needed on the host side (copies are staged)
   rc = dsfft_round_to(in, a.data(), count, p->precision);

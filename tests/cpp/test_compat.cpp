@@ -195,11 +195,25 @@ static void device_checks() {
     for (const auto& v : forward(p8, x, c)) any_nan = any_nan || std::isnan(v.re) || std::isnan(v.im);
     CHECK(any_nan);
   }
-  // fp64 plans are table-only on this path
+  // fp64 on the device: the reference's own fp64 tests verbatim
+  // (test_fft.cpp:110-128 oracle equivalence < 1e-11, 130-149 op accounting)
+  for (std::size_t n = 2; n <= 512; n <<= 1) {
+    const SampleBuffer x = random_buffer(n, 1000 + n);
+    const SampleBuffer ref = dft(x);
+    for (Strategy s : {Strategy::standard, Strategy::linzer_feig, Strategy::cosine,
+                       Strategy::dual_select}) {
+      ArithmeticContext c(Precision::fp64);
+      CHECK(rel_l2(forward(make_plan(n, s, Precision::fp64), x, c), ref) < 1e-11);
+    }
+  }
   {
-    const FftPlan p64 = make_plan(64, Strategy::dual_select, Precision::fp64);
+    const FftPlan p1024 = make_plan(1024, Strategy::dual_select, Precision::fp64);
     ArithmeticContext c(Precision::fp64);
-    CHECK_THROWS_AS(forward(p64, SampleBuffer(64), c), std::runtime_error);
+    const SampleBuffer x = random_buffer(1024, 8);
+    forward(p1024, x, c);
+    CHECK(c.counters().fma_count == 6 * 512 * 10);
+    const SampleBuffer back = inverse(p1024, forward(p1024, x, c), c);
+    CHECK(rel_l2(back, x) < 1e-13);
   }
 }
 

@@ -139,9 +139,35 @@ def test_errors(dsfft, cuda):
     bad = cuda.zeros((2, 32, 2), dtype=cuda.float32, device="cuda")
     with pytest.raises(ValueError, match="does not match plan size"):
         dsfft.forward(plan, bad)
-    p64 = dsfft.make_plan(64, "dual", "fp64")
-    with pytest.raises(NotImplementedError):
-        dsfft.forward_f64(p64, np.zeros(64, dtype=np.complex128))
+    with pytest.raises(ValueError, match="complex128"):
+        dsfft.forward(dsfft.make_plan(64, "dual", "fp64"), bad)
+
+
+@pytest.mark.parametrize("strategy", ALL_STRATEGIES)
+@pytest.mark.parametrize("n", [2 ** m for m in (1, 2, 3, 5, 6, 8, 10, 12, 14, 16)])
+@pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
+def test_fp64_bit_exact(dsfft, cuda, orc, n, strategy, inverse):
+    """Precision::fp64 (DFMA/DMUL/DADD per pass) == the reference's fp64."""
+    chk = _checker()
+    batch = 3
+    x = orc.random_buffer(n, 40960 + 2 * n, batch=batch)
+    plan = dsfft.make_plan(n, strategy, "fp64")
+    t = cuda.from_numpy(np.ascontiguousarray(x)).cuda()
+    y = dsfft.execute(plan, 1 if inverse else 0, t).cpu().numpy()
+    want = (chk.inverse if inverse else chk.forward)(x, strategy, "fp64")
+    assert bit_mismatches(y.view(np.float64), want.view(np.float64)) == 0
+
+
+def test_fp64_oracle_equivalence(dsfft, cuda, orc):
+    """test_fft.cpp:110-128 / acceptance criterion 5 through the device:
+    every strategy within rel-L2 1e-11 of the FP64 DFT, n <= 4096."""
+    for m in range(1, 13):
+        n = 2 ** m
+        x = orc.random_buffer(n, 40960 + 2 * n, batch=1)
+        ref = orc.dft(x)
+        for s in ALL_STRATEGIES:
+            y = dsfft.forward_f64(dsfft.make_plan(n, s, "fp64"), x)
+            assert orc.rel_l2(y, ref) < 1e-11, (n, s)
 
 
 LARGE = [2 ** m for m in range(13, 21)]

@@ -96,11 +96,9 @@ def test_no_cpu_fallback_without_device(dsfft):
         pytest.skip("device present")
     with pytest.raises(dsfft.DsfftError, match="no CPU fallback|not sm_100"):
         dsfft.make_plan(1024, "dual", "fp16")
-    # fp64 plans are table-only; executing them is refused, never emulated
-    p = dsfft.make_plan(64, "dual", "fp64")
-    assert p.table.size == 32
-    with pytest.raises(NotImplementedError):
-        dsfft.forward_f64(p, np.zeros(64, dtype=np.complex128))
+    # every precision runs on the device only, never emulated on the host
+    with pytest.raises(dsfft.DsfftError, match="no CPU fallback|not sm_100"):
+        dsfft.make_plan(64, "dual", "fp64")
 
 
 def test_schedule_dataflow_exact(tmp_path):
