@@ -43,7 +43,7 @@ DEFAULT_BATCH = 1 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsfft", choices=["dsfft", "reference"])
     ap.add_argument("--n", type=int, default=DEFAULT_N)
@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -263,9 +264,18 @@ def main():
     peak, peak_kind = load_peaks()
     traffic = load_traffic(args)
 
-    # accuracy on a sample of this run's outputs
-    idx = torch.arange(0, batch, max(1, batch // 256), device=dev)[:256]
-    max_err, med_err = accuracy_sample(y[idx].cpu().numpy(), x[idx].cpu().numpy(), n)
+    # accuracy of every transform of the batch, on the device: rel-L2 vs an
+    # FP64 reference transform (dsfft_error_device, measure_error semantics)
+    acc = None
+    if not args.no_accuracy:
+        rep = dsfft.error_device(plan, x, "forward")
+        acc = {"max_rel_l2_vs_fp64": rep["rel_l2_max"], "median_rel_l2": rep["rel_l2_median"],
+               "nonfinite": rep["nonfinite_trials"], "transforms": rep["trials"],
+               "how": "dsfft_error_device over the whole batch (FP64 reference transform)"}
+        # host cross-check on a few transforms: numpy FP64 FFT
+        idx = torch.arange(0, batch, max(1, batch // 16), device=dev)[:16]
+        acc["numpy_check_max"], _ = accuracy_sample(y[idx].cpu().numpy(), x[idx].cpu().numpy(),
+                                                    n)
 
     # e2e through the C ABI with pinned host buffers
     e2e = None
@@ -318,8 +328,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "fft_small_kernel",
                          "algorithmic_bytes_per_launch": algo_bytes},
-            "accuracy": {"max_rel_l2_vs_fp64_dft": max_err, "median_rel_l2": med_err,
-                         "sample": int(idx.numel())},
+            "accuracy": acc,
             "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),

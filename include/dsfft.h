@@ -122,6 +122,38 @@ int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int direction, cons
 int dsfft_execute_f64(dsfft_plan plan, int direction, const double* in, double* out,
                       size_t batch);
 
+/* == fmafft::ErrorReport (analysis.hpp:58-68). metric: 0 roundtrip,
+ * 1 forward_vs_oracle (ErrorMetric, analysis.hpp:49). */
+typedef struct {
+  uint64_t n;
+  int32_t strategy;
+  int32_t precision;
+  int32_t metric;
+  int32_t pad_;
+  uint64_t trials;
+  uint64_t seed;
+  double rel_l2_median;
+  double rel_l2_max;
+  uint64_t nonfinite_trials;
+} dsfft_error_report;
+
+/* Device error harness over a whole batch already on the device (working
+ * precision): per-transform relative_l2_error (analysis.cpp:41-57) of the
+ * forward against an FP64 reference transform, or of inverse(forward(x))
+ * against x; median over finite transforms, max (+inf if any non-finite) and
+ * the non-finite count (analysis.cpp:16-22,142-152).  `errs` (optional,
+ * `batch` doubles, host) receives the per-transform errors. */
+int dsfft_error_device(dsfft_plan plan, int metric, const void* d_x, size_t batch, void* stream,
+                       dsfft_error_report* out, double* errs);
+
+/* measure_error(n, strategy, precision, metric, trials, seed)
+ * (analysis.cpp:101-154): the reference's protocol (one SplitMix64 stream,
+ * re then im, ingest round_to) with every transform on `device`.  The FP64
+ * reference is the device fp64 transform instead of the O(n^2) dft_oracle
+ * (both FP64-accurate; errors agree to ~1e-9 relative). */
+int dsfft_measure_error(size_t n, int strategy, int precision, int metric, size_t trials,
+                        uint64_t seed, int device, dsfft_error_report* out);
+
 /* round_to (precision.cpp:61-75) of `count` doubles into the working format
  * (binary16 / binary32 words), and the exact widening back. */
 int dsfft_round_to(const double* in, void* out, size_t count, int precision);

@@ -279,3 +279,48 @@ def execute_multi(plans, direction: int, h_in: np.ndarray, h_out: np.ndarray,
     arr = (C.c_void_p * len(plans))(*[p._handle for p in plans])
     _check(lib.dsfft_execute_multi(C.cast(arr, C.c_void_p), len(plans), direction,
                                    h_in.ctypes.data, h_out.ctypes.data, batch))
+
+
+class _ErrorReport(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("strategy", C.c_int32), ("precision", C.c_int32),
+                ("metric", C.c_int32), ("pad_", C.c_int32), ("trials", C.c_uint64),
+                ("seed", C.c_uint64), ("rel_l2_median", C.c_double),
+                ("rel_l2_max", C.c_double), ("nonfinite_trials", C.c_uint64)]
+
+
+def _report(rep: "_ErrorReport") -> dict:
+    return {k: getattr(rep, k) for k, _ in _ErrorReport._fields_ if k != "pad_"}
+
+
+_METRICS = {"roundtrip": 0, "forward": 1, "forward_vs_oracle": 1}
+
+
+def error_device(plan: FftPlan, x, metric: str = "forward", stream=None,
+                 per_transform: bool = False):
+    """Device error harness over a device batch (dsfft_error_device): the
+    reference's ErrorReport (analysis.hpp:58-68) for every transform in `x`."""
+    import torch
+    batch = _torch_view(x, plan)
+    lib = _load()
+    lib.dsfft_error_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p,
+                                       C.POINTER(_ErrorReport), C.c_void_p]
+    rep = _ErrorReport()
+    errs = np.empty(batch, dtype=np.float64) if per_transform else None
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib.dsfft_error_device(plan._handle, _METRICS[metric], x.data_ptr(), batch, stream,
+                                  C.byref(rep), errs.ctypes.data if errs is not None else None))
+    return (_report(rep), errs) if per_transform else _report(rep)
+
+
+def measure_error(n: int, strategy: str, precision: str, metric: str = "forward",
+                  trials: int = 100, seed: int = 42, device: int = 0) -> dict:
+    """measure_error (analysis.cpp:101-154) with every transform on the device."""
+    lib = _load()
+    lib.dsfft_measure_error.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_size_t,
+                                        C.c_uint64, C.c_int, C.POINTER(_ErrorReport)]
+    rep = _ErrorReport()
+    _check(lib.dsfft_measure_error(int(n), STRATEGIES[parse_strategy(strategy)],
+                                   PRECISIONS[parse_precision(precision)], _METRICS[metric],
+                                   int(trials), int(seed), int(device), C.byref(rep)))
+    return _report(rep)

@@ -14,6 +14,7 @@
 
 #include "../../include/dsfft.h"
 #include "host_table.hpp"
+#include "error_harness.cuh"
 #include "fp64.cuh"
 #include "multipass.cuh"
 #include "small_launch.cuh"
@@ -109,6 +110,7 @@ struct dsfft_plan_s {
   size_t smem_optin = 0;
   std::mutex mu;
   HostPipe* pipe = nullptr;
+  dsfft::F64Plan* ref64 = nullptr;  // lazily built FP64 reference for the error harness
   uint8_t* scratch = nullptr;  // 16-byte-aligned tail staging (N=2 fp16, odd batch)
 };
 
@@ -341,6 +343,7 @@ int dsfft_plan_destroy(dsfft_plan p) {
     delete p->pipe;
     if (p->mp) dsfft::multipass_destroy(p->mp);
     if (p->f64) dsfft::fp64_destroy(p->f64);
+    if (p->ref64) dsfft::fp64_destroy(p->ref64);
   }
   delete p;
   return DSFFT_OK;
@@ -481,6 +484,123 @@ int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int dir, const void
   }
   g_launches = total;
   return DSFFT_OK;
+}
+
+int dsfft_error_device(dsfft_plan p, int metric, const void* d_x, size_t batch, void* stream_,
+                       dsfft_error_report* out, double* errs_out) {
+  g_launches = 0;
+  int rc = check_exec_args(p, DSFFT_FORWARD, d_x, const_cast<void*>(d_x));
+  if (rc) return rc;
+  if (metric != 0 && metric != 1) return fail(DSFFT_ERR_INVALID, "unknown metric");
+  if (batch == 0) return fail(DSFFT_ERR_INVALID, "trials must be >= 1");
+  DeviceGuard guard(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  if (metric == 1 && !p->ref64) {  // FP64 reference transform (any strategy is FP64-accurate)
+    p->ref64 = dsfft::fp64_create(dsfft::plan_table(p->n, DSFFT_DUAL_SELECT, DSFFT_FP64, 1e-7),
+                                  int(p->m), DSFFT_DUAL_SELECT);
+    if (!p->ref64) return fail(DSFFT_ERR_CUDA, dsfft::fp64_error());
+  }
+  const size_t n = p->n, tb = n * sample_bytes(p->precision);
+  const size_t chunk = std::max<size_t>(1, (size_t(256) << 20) / (n * sizeof(double2)));
+  void *y = nullptr, *z = nullptr;
+  double2 *ax = nullptr, *bx = nullptr;
+  double* derr = nullptr;
+  const size_t cb = std::min(chunk, batch);
+  auto cleanup = [&] {
+    cudaFree(y);
+    cudaFree(z);
+    cudaFree(ax);
+    cudaFree(bx);
+    cudaFree(derr);
+  };
+  if (cudaMalloc(&y, cb * tb) != cudaSuccess || cudaMalloc(&z, cb * tb) != cudaSuccess ||
+      cudaMalloc(&ax, cb * n * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc(&bx, cb * n * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc(&derr, cb * sizeof(double)) != cudaSuccess) {
+    cleanup();
+    cudaGetLastError();
+    return fail(DSFFT_ERR_CUDA, "error harness: device allocation failed");
+  }
+  std::vector<double> errs(batch);
+  uint64_t launches = 0;
+  for (size_t b0 = 0; b0 < batch && rc == DSFFT_OK; b0 += chunk) {
+    const size_t nb = std::min(chunk, batch - b0);
+    const void* x = static_cast<const uint8_t*>(d_x) + b0 * tb;
+    rc = launch(p, DSFFT_FORWARD, x, y, nb, st);  // the measured transform
+    launches += g_launches;
+    g_launches = 0;
+    if (rc) break;
+    if (metric == 1) {  // forward vs FP64 reference of the ingested input
+      if (dsfft::launch_widen(x, bx, (long long)(nb * n), p->precision, st) ||
+          dsfft::fp64_execute(*p->ref64, false, bx, ax, nb, 0.0, p->sm_count, st, &launches) ||
+          dsfft::launch_widen(y, bx, (long long)(nb * n), p->precision, st))
+        rc = fail(DSFFT_ERR_CUDA, "error harness: reference transform failed");
+    } else {  // roundtrip: inverse(forward(x)) vs x
+      rc = launch(p, DSFFT_INVERSE, y, z, nb, st);
+      launches += g_launches;
+      g_launches = 0;
+      if (!rc && (dsfft::launch_widen(z, bx, (long long)(nb * n), p->precision, st) ||
+                  dsfft::launch_widen(x, ax, (long long)(nb * n), p->precision, st)))
+        rc = fail(DSFFT_ERR_CUDA, "error harness: widening failed");
+    }
+    if (rc) break;
+    if (dsfft::launch_rel_l2(bx, ax, derr, (long long)n, (long long)nb, st) ||
+        cudaMemcpyAsync(errs.data() + b0, derr, nb * sizeof(double), cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      rc = fail(DSFFT_ERR_CUDA, "error harness: reduction failed");
+  }
+  cleanup();
+  if (rc) return rc;
+  const dsfft::ErrorStats s = dsfft::aggregate_errors(errs);
+  if (s.invalid) return fail(DSFFT_ERR_INVALID, "relative_l2_error: all-zero reference");
+  if (out) {
+    *out = dsfft_error_report{};
+    out->n = p->n;
+    out->strategy = p->strategy;
+    out->precision = p->precision;
+    out->metric = metric;
+    out->trials = batch;
+    out->rel_l2_median = s.median;
+    out->rel_l2_max = s.max;
+    out->nonfinite_trials = s.nonfinite;
+  }
+  if (errs_out) std::memcpy(errs_out, errs.data(), batch * sizeof(double));
+  g_launches = launches;
+  return DSFFT_OK;
+}
+
+int dsfft_measure_error(size_t n, int strategy, int precision, int metric, size_t trials,
+                        uint64_t seed, int device, dsfft_error_report* out) {
+  if (trials < 1) return fail(DSFFT_ERR_INVALID, "trials must be >= 1");
+  dsfft_plan p = nullptr;
+  int rc = dsfft_plan_create(n, strategy, precision, 1e-7, device, &p);
+  if (rc) return rc;
+  DeviceGuard guard(device);
+  // the reference protocol: one SplitMix64 stream, 2n draws per trial, re then
+  // im, uniform [-1, 1) (analysis.hpp:73-91, analysis.cpp:120-125), then
+  // ingest-rounded (analysis.cpp:126-130)
+  uint64_t state = seed;
+  auto next = [&state]() {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  std::vector<double> draws(2 * n * trials);
+  for (double& d : draws) d = 2.0 * (static_cast<double>(next() >> 11) * 0x1p-53) - 1.0;
+  const size_t tb = n * sample_bytes(precision);
+  std::vector<uint8_t> host(tb * trials);
+  rc = dsfft_round_to(draws.data(), host.data(), draws.size(), precision);
+  void* d_x = nullptr;
+  if (!rc && cudaMalloc(&d_x, host.size()) != cudaSuccess) rc = fail(DSFFT_ERR_CUDA, "alloc");
+  if (!rc && cudaMemcpy(d_x, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(DSFFT_ERR_CUDA, "upload");
+  if (!rc) rc = dsfft_error_device(p, metric, d_x, trials, nullptr, out, nullptr);
+  if (!rc && out) out->seed = seed;
+  if (d_x) cudaFree(d_x);
+  dsfft_plan_destroy(p);
+  return rc;
 }
 
 int dsfft_round_to(const double* in, void* out, size_t count, int precision) {
