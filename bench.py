@@ -159,6 +159,17 @@ def cpu_reference_rate(args, seconds: float, threads: int = 0):
     return count / dt, count, kind, cores, dt
 
 
+def workload_config(args, world):
+    """The same config block on both arms (BASELINE configs[1] by default)."""
+    which = "configs[1]" if args.n == 1024 and args.precision == "fp16" else \
+        ("configs[4]" if args.n > 4096 else "configs[2]")
+    return {"workload": f"N={args.n} {args.precision} {args.strategy}-select forward, "
+                        f"batch {args.batch} per GPU (BASELINE {which})",
+            "n": args.n, "precision": args.precision, "strategy": args.strategy,
+            "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+            "l2": "inputs (and outputs) > L2 per step; no flush needed"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path timed on this host's cores."""
     if rank != 0:
@@ -178,9 +189,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": 1e3 * sample / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f16" if args.precision == "fp16" else "f32", "data": "synthetic",
-        "config": {"workload": f"N={args.n} {args.precision} {args.strategy}-select forward",
-                   "n": args.n, "precision": args.precision, "strategy": args.strategy,
-                   "global_batch": args.batch * args.gpus},
+        "config": workload_config(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": cores, "kind": kind,
                          "sample": f"{sample} transforms of the workload per step"},
         "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0,
@@ -317,11 +326,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f16" if prec == "fp16" else "f32", "data": "synthetic",
-            "config": {"workload": f"N={n} {prec} {args.strategy}-select forward, batch {batch}"
-                                   " per GPU (BASELINE configs[1])",
-                       "n": n, "precision": prec, "strategy": args.strategy,
-                       "batch_per_gpu": batch, "global_batch": total,
-                       "l2": "inputs (and outputs) > L2 per step; no flush needed"},
+            "config": workload_config(args, world),
             "gflops": 5.0 * n * np.log2(n) * value / 1e9,
             "hbm_gbs": achieved * world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
