@@ -225,15 +225,31 @@ def main():
     import torch
     import paper_2604_00567_b200 as dsfft
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; DSFFT_DIST_BACKEND=gloo exercises the control plane
+    # with several ranks sharing one device (no data-path collective either way)
+    backend = os.environ.get("DSFFT_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def reduce_max(v: float) -> float:
+        """Control-plane MAX over ranks (NCCL tensors live on the device)."""
+        if not dist:
+            return float(v)
+        t = torch.tensor([float(v)], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     n, batch, prec = args.n, args.batch, args.precision
-    plan = dsfft.make_plan(n, args.strategy, prec, device=local)
+    plan = dsfft.make_plan(n, args.strategy, prec, device=local_dev)
     wdt = torch.float16 if prec == "fp16" else torch.float32
     sbytes = 4 if prec == "fp16" else 8
     g = torch.Generator(device=dev)
@@ -261,11 +277,7 @@ def main():
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max(ev0.elapsed_time(ev1) / args.steps)  # the job's step = slowest rank
     total = batch * world
     value = total / (ms * 1e-3)
     algo_bytes = 2.0 * n * sbytes * batch  # per launch, read once + write once
@@ -290,8 +302,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         ksteps = args.e2e_steps or max(2, min(args.steps, 5))
-        hx = x.cpu().pin_memory()
-        hy = torch.empty_like(hx).pin_memory()
+        hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        hx.copy_(x)
+        hy = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         hxn, hyn = hx.numpy(), hy.numpy()
         dsfft.execute_host(plan, 0, hxn, hyn, batch, stream.cuda_stream)  # warm-up
         if dist:
@@ -299,11 +312,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(ksteps):
             dsfft.execute_host(plan, 0, hxn, hyn, batch, stream.cuda_stream)
-        dt = (time.perf_counter() - t0) / ksteps
-        if dist:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = reduce_max((time.perf_counter() - t0) / ksteps)
         e2e = {"value": total / dt, "unit": "transforms/s",
                "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
                "d2h_bytes_per_step": int(hy.numel() * hy.element_size()),
