@@ -405,7 +405,8 @@ int dsfft_execute_host(dsfft_plan p, int dir, const void* h_in, void* h_out, siz
   std::lock_guard<std::mutex> lock(p->mu);
   cudaStream_t user = static_cast<cudaStream_t>(stream_);
   const size_t tb = p->n * sample_bytes(p->precision);
-  const size_t want_chunk = size_t(env_int("DSFFT_HOST_CHUNK_MB", 32)) << 20;
+  // 64 MiB chunks: ~96 GB/s H2D+D2H on PCIe Gen5 x16 (16 MiB: 85, 256 MiB: 93)
+  const size_t want_chunk = size_t(env_int("DSFFT_HOST_CHUNK_MB", 64)) << 20;
   size_t per = std::max<size_t>(1, want_chunk / tb);
   if (per % 2) per += (per > 1) ? -1 : 1;  // keep fp16 pairs whole
   const size_t chunk_bytes = per * tb;
