@@ -18,6 +18,7 @@
 #include "fp64.cuh"
 #include "multipass.cuh"
 #include "small_launch.cuh"
+#include "stream_alloc.cuh"
 
 namespace {
 
@@ -39,12 +40,14 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
   } while (0)
 
-// Restores the caller's current device on scope exit.
+// Makes `dev`'s primary context current on this thread (always: a fresh host
+// thread has no current context, which the driver-API tensor-map encoder
+// needs) and restores the caller's device on scope exit.
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
     cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
+    cudaSetDevice(dev);
   }
   ~DeviceGuard() {
     int cur = -1;
@@ -111,7 +114,6 @@ struct dsfft_plan_s {
   std::mutex mu;
   HostPipe* pipe = nullptr;
   dsfft::F64Plan* ref64 = nullptr;  // lazily built FP64 reference for the error harness
-  uint8_t* scratch = nullptr;  // 16-byte-aligned tail staging (N=2 fp16, odd batch)
 };
 
 namespace {
@@ -221,15 +223,22 @@ int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
     ++g_launches;
   }
   if (main_batch != batch) {
-    if (!p->scratch) DSFFT_CUDA(cudaMalloc(&p->scratch, 64));
+    uint8_t* scratch = nullptr;  // stream-ordered: safe when a plan runs on several streams
+    DSFFT_CUDA(dsfft::scratch_alloc(reinterpret_cast<void**>(&scratch), 64, stream));
+    struct Release {
+      uint8_t* s;
+      cudaStream_t st;
+      ~Release() { dsfft::scratch_free(s, st); }
+    } release{scratch, stream};
     const size_t off = main_batch * tb;
-    DSFFT_CUDA(cudaMemcpyAsync(p->scratch, static_cast<const uint8_t*>(in) + off, tb,
+    DSFFT_CUDA(cudaMemsetAsync(scratch, 0, 64, stream));
+    DSFFT_CUDA(cudaMemcpyAsync(scratch, static_cast<const uint8_t*>(in) + off, tb,
                                cudaMemcpyDeviceToDevice, stream));
     dsfft::LaunchArgs a{};
     a.standard = p->strategy == DSFFT_STANDARD;
     a.inverse = dir == DSFFT_INVERSE;
-    a.kp.in = p->scratch;
-    a.kp.out = p->scratch;
+    a.kp.in = scratch;
+    a.kp.out = scratch;
     a.kp.tw = p->d_tw;
     a.kp.batch = 2;  // pad to a 16-byte transfer; the second transform is discarded
     a.kp.n_items = 1;
@@ -241,7 +250,7 @@ int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
     cudaError_t e = p->small->launch(a);
     if (e != cudaSuccess) return cuda_fail(e, "fft_small_kernel launch (tail)");
     ++g_launches;
-    DSFFT_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(out) + off, p->scratch, tb,
+    DSFFT_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(out) + off, scratch, tb,
                                cudaMemcpyDeviceToDevice, stream));
   }
   return DSFFT_OK;
@@ -339,7 +348,6 @@ int dsfft_plan_destroy(dsfft_plan p) {
   {
     DeviceGuard guard(p->device);
     if (p->d_tw) cudaFree(p->d_tw);
-    if (p->scratch) cudaFree(p->scratch);
     delete p->pipe;
     if (p->mp) dsfft::multipass_destroy(p->mp);
     if (p->f64) dsfft::fp64_destroy(p->f64);
@@ -496,9 +504,12 @@ int dsfft_error_device(dsfft_plan p, int metric, const void* d_x, size_t batch, 
   if (batch == 0) return fail(DSFFT_ERR_INVALID, "trials must be >= 1");
   DeviceGuard guard(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  if (metric == 1 && !p->ref64) {  // FP64 reference transform (any strategy is FP64-accurate)
-    p->ref64 = dsfft::fp64_create(dsfft::plan_table(p->n, DSFFT_DUAL_SELECT, DSFFT_FP64, 1e-7),
-                                  int(p->m), DSFFT_DUAL_SELECT);
+  if (metric == 1) {  // FP64 reference transform (any strategy is FP64-accurate)
+    std::lock_guard<std::mutex> lock(p->mu);
+    if (!p->ref64)
+      p->ref64 = dsfft::fp64_create(
+          dsfft::plan_table(p->n, DSFFT_DUAL_SELECT, DSFFT_FP64, 1e-7), int(p->m),
+          DSFFT_DUAL_SELECT);
     if (!p->ref64) return fail(DSFFT_ERR_CUDA, dsfft::fp64_error());
   }
   const size_t n = p->n, tb = n * sample_bytes(p->precision);

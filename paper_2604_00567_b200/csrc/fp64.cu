@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "fp64.cuh"
+#include "stream_alloc.cuh"
 
 namespace dsfft {
 
@@ -34,12 +35,8 @@ struct Rec64 {
 struct F64Plan {
   int m = 0, strategy = 0;
   Rec64* d_tab = nullptr;
-  double2* scratch[2] = {nullptr, nullptr};
-  size_t scratch_bytes = 0;
   ~F64Plan() {
     if (d_tab) cudaFree(d_tab);
-    for (auto* s : scratch)
-      if (s) cudaFree(s);
   }
 };
 
@@ -117,25 +114,29 @@ int fp64_execute(F64Plan& fp, bool inverse, const void* in, void* out, size_t ba
                  double scale, int sm_count, cudaStream_t st, uint64_t* launches) {
   const int m = fp.m;
   const size_t bytes = (size_t(1) << m) * sizeof(double2) * batch;
-  if (m > 1 && fp.scratch_bytes < bytes) {
-    for (auto*& s : fp.scratch) {
-      if (s) cudaFree(s);
-      s = nullptr;
-    }
-    fp.scratch_bytes = 0;
-    for (auto*& s : fp.scratch)
-      if (cudaMalloc(&s, bytes) != cudaSuccess) {
+  // per-call, stream-ordered ping-pong buffers (plans may run on several streams)
+  double2* scratch[2] = {nullptr, nullptr};
+  if (m > 1)
+    for (auto*& sp : scratch)
+      if (scratch_alloc(reinterpret_cast<void**>(&sp), bytes, st) != cudaSuccess) {
+        scratch_free(scratch[0], st);
         g_f64_err = "fp64: scratch allocation failed";
         return 1;
       }
-    fp.scratch_bytes = bytes;
-  }
+  struct Release {
+    double2** s;
+    cudaStream_t st;
+    ~Release() {
+      scratch_free(s[0], st);
+      scratch_free(s[1], st);
+    }
+  } release{scratch, st};
   const long long total = (long long)batch << (m - 1);
   const int grid = int(std::min<long long>((total + 255) / 256, (long long)sm_count * 8));
   const bool std_ = fp.strategy == kStandard;
   for (int p = 0; p < m; ++p) {
-    const double2* X = p == 0 ? static_cast<const double2*>(in) : fp.scratch[(p - 1) & 1];
-    double2* Y = p == m - 1 ? static_cast<double2*>(out) : fp.scratch[p & 1];
+    const double2* X = p == 0 ? static_cast<const double2*>(in) : scratch[(p - 1) & 1];
+    double2* Y = p == m - 1 ? static_cast<double2*>(out) : scratch[p & 1];
     const bool ci = inverse && p == 0, so = inverse && p == m - 1;
     auto go = [&](auto kern) { kern<<<grid, 256, 0, st>>>(X, Y, fp.d_tab, total, m, p, scale); };
     if (std_) {

@@ -33,6 +33,7 @@
 
 #include "fft_kernels.cuh"
 #include "multipass.cuh"
+#include "stream_alloc.cuh"
 
 namespace dsfft {
 
@@ -338,13 +339,10 @@ struct MultipassPlan {
   int m = 0, strategy = 0, precision = 0, sm_count = 0;
   size_t smem_optin = 0;
   std::vector<MpGroup> groups;
-  uint8_t* scratch[2] = {nullptr, nullptr};
   size_t chunk_transforms = 0;
   ~MultipassPlan() {
     for (auto& g : groups)
       if (g.d_tw) cudaFree(g.d_tw);
-    for (auto* s : scratch)
-      if (s) cudaFree(s);
   }
 };
 
@@ -378,10 +376,10 @@ std::vector<int> split_passes(int m, int max_s) {
 size_t sample_bytes(int precision) { return precision == kFp16 ? 4 : 8; }
 
 // Input map of a pass group over `batch` transforms starting at `base`.
-bool make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
-                 long long batch) {
+int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
+                long long batch) {
   EncodeFn enc = encode_fn();
-  if (!enc) return false;
+  if (!enc) return -1;
   const CUtensorMapDataType dt =
       vb == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64;
   const cuuint64_t N = cuuint64_t(1) << m;
@@ -404,7 +402,7 @@ bool make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
-  return r == CUDA_SUCCESS;
+  return int(r);
 }
 
 template <int S1, class A, bool STD>
@@ -522,13 +520,6 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   // per-launch ramp/tail than they gain from L2 residency; 1 GiB chunks win
   const size_t want = size_t(env && *env ? std::atoi(env) : 1024) << 20;
   mp->chunk_transforms = std::max<size_t>(1, want / tb);
-  const size_t bytes = mp->chunk_transforms * tb;
-  for (auto*& s : mp->scratch)
-    if (cudaMalloc(&s, bytes) != cudaSuccess) {
-      g_mp_err = "multipass: scratch allocation failed";
-      delete mp;
-      return nullptr;
-    }
   return mp;
 }
 
@@ -541,14 +532,36 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const bool f16 = mp.precision == kFp16;
   const bool std_ = mp.strategy == kStandard;
   const int ng = int(mp.groups.size());
+  // per-call, stream-ordered intermediates (plans may run on several streams)
+  const size_t chunk = std::min(mp.chunk_transforms, batch);
+  uint8_t* scratch[2] = {nullptr, nullptr};
+  for (int i = 0; i < std::min(ng - 1, 2); ++i)
+    if (scratch_alloc(reinterpret_cast<void**>(&scratch[i]), chunk * tb, stream) !=
+        cudaSuccess) {
+      for (auto* sp : scratch) scratch_free(sp, stream);
+      g_mp_err = "multipass: scratch allocation failed";
+      return 1;
+    }
+  struct Release {
+    uint8_t** s;
+    cudaStream_t st;
+    ~Release() {
+      scratch_free(s[0], st);
+      scratch_free(s[1], st);
+    }
+  } release{scratch, stream};
   // maps: the user input over the whole batch (chunk = coordinate offset) and
-  // the two fixed scratch buffers
+  // the scratch buffers
   std::vector<CUtensorMap> maps(ng);
   for (int i = 0; i < ng; ++i) {
-    const void* base = i == 0 ? in : mp.scratch[(i - 1) & 1];
-    const long long nb = i == 0 ? (long long)batch : (long long)mp.chunk_transforms;
-    if (!make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s, vb, nb)) {
-      g_mp_err = "multipass: cuTensorMapEncodeTiled failed";
+    const void* base = i == 0 ? in : scratch[(i - 1) & 1];
+    const long long nb = i == 0 ? (long long)batch : (long long)chunk;
+    const int rc = make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s, vb, nb);
+    if (rc != 0) {
+      g_mp_err = "multipass: cuTensorMapEncodeTiled failed (CUresult " + std::to_string(rc) +
+                 ", group " + std::to_string(i) + ", base " +
+                 std::to_string(reinterpret_cast<uintptr_t>(base)) + ", batch " +
+                 std::to_string(nb) + ")";
       return 1;
     }
   }
@@ -557,7 +570,7 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
     for (int i = 0; i < ng; ++i) {
       const MpGroup& g = mp.groups[i];
       MpParams p{};
-      p.out = i == ng - 1 ? static_cast<uint8_t*>(out) + b0 * tb : mp.scratch[i & 1];
+      p.out = i == ng - 1 ? static_cast<uint8_t*>(out) + b0 * tb : scratch[i & 1];
       p.tw = g.d_tw;
       p.m = mp.m;
       p.P = g.P;

@@ -213,6 +213,40 @@ def test_multipass_many_chunks(dsfft, cuda, orc):
     assert bit_mismatches(y[idx], want) == 0
 
 
+@pytest.mark.parametrize("n,precision", [(1024, "fp16"), (1 << 16, "fp16"), (1 << 14, "fp32"),
+                                         (256, "fp64"), (2, "fp16")])
+def test_one_plan_many_streams(dsfft, cuda, orc, n, precision):
+    """Plans are shareable (fft.hpp:14-16): one plan executed concurrently on
+    two streams from two host threads gives the single-stream bits."""
+    import threading
+    torch = cuda
+    batch = 9 if n < (1 << 14) else 4
+    x = ref_inputs(orc, n, batch, seed=n + 1, precision=precision if precision != "fp64" else
+                   "fp64")
+    xw = x if precision == "fp64" else to_work(x, precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    ins = [torch.from_numpy(np.ascontiguousarray(xw)).cuda() for _ in range(2)]
+    outs = [torch.empty_like(ins[0]) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+
+    def work(i):
+        for _ in range(3):
+            dsfft.forward(plan, ins[i], out=outs[i], stream=streams[i].cuda_stream)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    want = _checker().forward(x, "dual", precision)
+    want = want if precision == "fp64" else to_work(want, precision)
+    for o in outs:
+        got = o.cpu().numpy()
+        assert bit_mismatches(got.view(np.float64) if precision == "fp64" else got,
+                              want.view(np.float64) if precision == "fp64" else want) == 0
+
+
 def test_execute_multi_partitioner(dsfft, cuda, orc):
     """dsfft_execute_multi: contiguous shards on each listed device (here the
     one B200 twice, two host threads) reproduce the single-call result."""
