@@ -34,10 +34,11 @@ using CfgC = CfgW;
 // 32 values per thread over 2 warps: (E=64, 1 warp) needed ~210 registers and
 // 33 KB per group, leaving ~4 resident warps per SM
 using CfgW = Sched<11, 5, 2, 5, 5, 1>;
-using CfgC = CfgW;
+// one-word values: 64 per thread is ~64 data registers, so two stages fit
+using CfgC = Sched<11, 6, 1, 5, 6>;
 #elif DSFFT_M == 12
 using CfgW = Sched<12, 5, 4, 5, 5, 2>;
-using CfgC = CfgW;
+using CfgC = Sched<12, 6, 2, 6, 6>;
 #else
 #error "single-kernel path covers N <= 4096"
 #endif
@@ -53,7 +54,7 @@ SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   // fp16 one-complex-per-register wins for N <= 512 (94% of HBM at 512),
   // transform pairs for N >= 1024 (98% at 1024); N >= 2048 is shared-memory
   // bound (twiddles ~N*16 B), where a 1-deep ring with more groups wins.
-  e.f16_default = DSFFT_M >= 10 ? kVarF16P : kVarF16C;
+  e.f16_default = (DSFFT_M == 10 || DSFFT_M == 12) ? kVarF16P : kVarF16C;
   e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : 3;
   e.stages[kVarF16P] = DSFFT_M >= 11 ? 1 : 2;
   e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : 2;
