@@ -81,245 +81,233 @@ struct MpLayout {
   __host__ __device__ static constexpr int tw_bytes(bool first) {
     return ((first ? mp_first_records(S1) * 16 : kSlabRecords * 16) + 127) & ~127;
   }
-  static size_t smem_bytes(bool first, int stages) {
+  static size_t smem_bytes(bool first, int stages, int groups) {
     const int tw = tw_bytes(first);
-    return size_t(tw) + size_t(stages) * kBufBytes + size_t(stages) * 8;
+    return size_t(tw) + size_t(groups) * stages * (kBufBytes + 8);
   }
 };
 
-template <int S1, class A>
-constexpr int mp_min_blocks() {
-  // one-word values fit ~80 registers; two-word ~128
-  return 65536 / ((32 << S1) * (A::kWords == 1 ? 80 : 128)) > 0
-             ? 65536 / ((32 << S1) * (A::kWords == 1 ? 80 : 128))
-             : 1;
-}
-
+// One pass group over all tiles of a chunk.  A CTA runs G = blockDim/T tile
+// groups of T = 32 * 2^S1 threads; each thread owns 32 values in stage 1 and
+// 2^(5-S1) groups of 2^S1 in stage 2.  The CTA's contiguous tile range is
+// walked unit by unit (a unit = one column block tt, a range of transforms);
+// later pass groups stage the unit's twiddle slab once, shared by all groups,
+// and group g takes transforms b0+g, b0+g+G, ... of the unit with its own TMA
+// ring.  Register budget: one-word values ~80, two-word ~128.
 template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST>
-__global__ void __launch_bounds__(32 << S1, mp_min_blocks<S1, A>())
+__global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     mp_kernel(const __grid_constant__ CUtensorMap in_map, const MpParams p) {
   using Lay = MpLayout<S1, A>;
   constexpr int L = Lay::L, T = Lay::T, NG2 = 32 >> S1, VB = Lay::VB;
   constexpr int STRIDE = L + 1;  // padded exchange column (values)
   constexpr int ROWS_BOX = L < 256 ? L : 256;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = blockDim.x / T;
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int lane = t & 31, warp = t >> 5;
   const int S = p.stages;
   const int P = p.P;
   const long long N = 1LL << p.m;
   constexpr int tw_bytes = Lay::tw_bytes(FIRST);
   uint4* tws = reinterpret_cast<uint4*>(smem);
   const uint32_t tw_base = ptx::smem_u32(smem);
-  uint8_t* bufs = smem + tw_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + size_t(S) * Lay::kBufBytes);
+  uint8_t* bufs = smem + tw_bytes + size_t(g) * S * Lay::kBufBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tw_bytes + size_t(G) * S * Lay::kBufBytes) +
+                   g * S;
   const long long rblocks = FIRST ? 1 : ((1LL << P) >> 5);
+  const bool leader = t == 0;
+  auto group_sync = [&]() {
+    if (T == 32) __syncwarp(); else ptx::named_bar_sync(1 + g, T);
+  };
 
   if constexpr (FIRST) {  // column-independent twiddles: stage once per CTA
-    for (int i = threadIdx.x; i < mp_first_records(S1); i += T) tws[i] = p.tw[i];
+    for (int i = threadIdx.x; i < mp_first_records(S1); i += blockDim.x) tws[i] = p.tw[i];
   }
-  if (threadIdx.x == 0)
-    for (int b = 0; b < S; ++b) ptx::mbar_init(&bars[b], 1);
+  if (leader)
+    for (int i = 0; i < S; ++i) ptx::mbar_init(&bars[i], 1);
   ptx::fence_mbar_init();
   __syncthreads();
 
   const long long per = (p.tiles + gridDim.x - 1) / gridDim.x;
   const long long t_begin = blockIdx.x * per;
   const long long t_end = t_begin + per < p.tiles ? t_begin + per : p.tiles;
-  const bool leader = threadIdx.x == 0;
   uint64_t pol = 0;
   if (leader) pol = ptx::policy_evict_first();
-  auto issue_load = [&](long long tile, int slot) {
-    const long long tt = tile / p.nb;
-    const int b = int(tile - tt * p.nb + p.b_off);
+  const int nb = int(p.nb);
+  // TMA load of transform b of column block (q, rb) into ring slot `slot`
+  auto issue_load = [&](long long q, int rb, int b, int slot) {
     uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
     ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
 #pragma unroll
     for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
-      if constexpr (FIRST) {
-        ptx::tma_load_3d(dst + size_t(r0) * 32 * VB, &in_map, int(tt * 32), r0, b, &bars[slot],
-                         pol);
-      } else {
-        const long long q = tt / rblocks;
-        const int rb = int(tt - q * rblocks);
-        ptx::tma_load_4d(dst + size_t(r0) * 32 * VB, &in_map, rb * 32, int(q), r0, b,
-                         &bars[slot], pol);
-      }
+      if constexpr (FIRST)
+        ptx::tma_load_3d(dst + size_t(r0) * 32 * VB, &in_map, int(q * 32), r0,
+                         int(b + p.b_off), &bars[slot], pol);
+      else
+        ptx::tma_load_4d(dst + size_t(r0) * 32 * VB, &in_map, rb * 32, int(q), r0,
+                         int(b + p.b_off), &bars[slot], pol);
     }
   };
-  if (leader)
-    for (int i = 0; i < S && t_begin + i < t_end; ++i) issue_load(t_begin + i, i);
 
-  long long staged_rb = -1;
-  // tile -> (tt, b) and tt -> (q, rb), advanced incrementally (no divisions)
-  const int nb = int(p.nb);
-  int b = int(t_begin % nb);
-  long long tt = t_begin / nb;
-  long long q = FIRST ? tt : tt / rblocks;
-  int rb = FIRST ? 0 : int(tt - q * rblocks);
-  int it = 0, it_slot = 0;
-  uint32_t it_phase = 0;
-  for (long long tile = t_begin; tile < t_end; ++tile, ++it) {
-    if (it > 0 && ++it_slot == S) {
-      it_slot = 0;
-      it_phase ^= 1;
+  long long it = 0;  // this group's running tile count (ring slot / phase)
+  for (long long u0 = t_begin; u0 < t_end;) {
+    const long long tt = u0 / nb;  // column block of this unit
+    const int b0 = int(u0 - tt * nb);
+    const long long u1 = (tt + 1) * nb < t_end ? (tt + 1) * nb : t_end;
+    const int b1 = b0 + int(u1 - u0);
+    u0 = u1;
+    const long long q = FIRST ? tt : tt / rblocks;
+    const int rb = FIRST ? 0 : int(tt - q * rblocks);
+    if constexpr (!FIRST) {  // the unit's twiddle slab, shared by every group
+      __syncthreads();
+      const uint4* src = p.tw + (long long)rb * mp_block_records(S1);
+      for (int i = threadIdx.x; i < Lay::kSlabRecords; i += blockDim.x) tws[i] = src[i];
+      __syncthreads();
     }
-    if (it > 0 && ++b == nb) {
-      b = 0;
-      ++tt;
-      if constexpr (FIRST) {
-        q = tt;
-      } else if (++rb == rblocks) {
-        rb = 0;
-        ++q;
-      }
-    }
-    const int slot = it_slot;
-    if constexpr (!FIRST) {
-      if (rb != staged_rb) {  // new column block: stage its stage-1 twiddles
-        __syncthreads();
-        const uint4* src = p.tw + (long long)rb * mp_block_records(S1);
-        for (int i = threadIdx.x; i < Lay::kSlabRecords; i += T) tws[i] = src[i];
-        __syncthreads();
-        staged_rb = rb;
-      }
-    }
-    uint8_t* bp = bufs + size_t(slot) * Lay::kBufBytes;
-    const uint32_t buf = ptx::smem_u32(bp);
-    ptx::mbar_wait(&bars[slot], it_phase);
+    const int k = b1 - b0 > g ? (b1 - b0 - g + G - 1) / G : 0;  // this group's tiles
+    if (leader)
+      for (int i = 0; i < S && i < k; ++i) issue_load(q, rb, b0 + g + G * i, int((it + i) % S));
+    for (int i = 0; i < k; ++i) {
+      const int b = b0 + g + G * i;
+      const int slot = int((it + i) % S);
+      const uint32_t buf = ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes);
+      ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
 
-    uint32_t re[32], im[32];
-    // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) ----
+      uint32_t re[32], im[32];
+      // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) --
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
-      if constexpr (A::kWords == 1) {
-        re[c] = ptx::lds32(a);
-        if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
-      } else {
-        ptx::lds64(a, re[c], im[c]);
-        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
-      }
-    }
-#pragma unroll
-    for (int pl = 0; pl < 5; ++pl) {
-      uint32_t nre[32], nim[32];
-#pragma unroll
-      for (int rl = 0; rl < (1 << pl); ++rl) {
-        const int slot1 = (1 << pl) - 1 + rl;
-        const uint4 tw = FIRST ? ptx::lds128(tw_base + slot1 * 16)
-                               : ptx::lds128(tw_base + (slot1 * 32 + lane) * 16);
-#pragma unroll
-        for (int qq = 0; qq < (16 >> pl); ++qq) {
-          const int jl = (qq << pl) | rl;
-          const int oa = (qq << (pl + 1)) + rl;
-          butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa], nim[oa],
-                                 nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        re[i] = nre[i];
-        if constexpr (A::kWords == 2) im[i] = nim[i];
-      }
-    }
-    // ---- exchange through the padded slot: [col][local pos] -----------------
-    __syncthreads();  // every stage-1 read of the TMA tile is done
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
-      if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
-    }
-    __syncthreads();
-    // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
-    // column output), later groups lanes walk columns (contiguous rows)
-#pragma unroll
-    for (int j = 0; j < NG2; ++j) {
-      const int col = FIRST ? warp + (j << S1) : lane;
-      const int rl_ = FIRST ? lane : warp + (j << S1);
-#pragma unroll
-      for (int c = 0; c < (1 << S1); ++c) {
-        const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
-        const int v = (j << S1) + c;
-        if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
-      }
-    }
-    // release the slot to the tile S ahead
-    ptx::fence_proxy_async_smem();
-    __syncthreads();
-    if (leader && tile + S < t_end) issue_load(tile + S, slot);
-    // ---- stage 2 ------------------------------------------------------------
-    const uint4* tw2 = FIRST ? nullptr
-                             : p.tw + (long long)rb * mp_block_records(S1) + 31 * 32 +
-                                   warp * 32 + lane;
-#pragma unroll
-    for (int pl = 0; pl < S1; ++pl) {
-      uint32_t nre[32], nim[32];
-#pragma unroll
-      for (int rl = 0; rl < (1 << pl); ++rl)
-#pragma unroll
-        for (int j = 0; j < NG2; ++j) {
-          const int slot2 = (1 << pl) - 1 + rl;
-          uint4 tw;
-          if constexpr (FIRST)
-            tw = ptx::lds128(tw_base + (31 + (slot2 << 5) + lane) * 16);
-          else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
-            tw = ptx::lds128(tw_base + (31 * 32 + (warp << 5) + lane +
-                                        (((slot2 << 5) + (j << S1)) << 5)) * 16);
-          else  // r_l = warp + 2^S1 j
-            tw = __ldg(tw2 + ((slot2 << 5) + (j << S1)) * 32);
-#pragma unroll
-          for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
-            const int jl = (qq << pl) | rl;
-            const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
-            const int oa = (j << S1) + (qq << (pl + 1)) + rl;
-            butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
-                                   nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-          }
-        }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        re[i] = nre[i];
-        if constexpr (A::kWords == 2) im[i] = nim[i];
-      }
-    }
-    // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') --------------------------
-    uint8_t* gout = p.out + b * N * VB;
-    uint8_t* base;
-    long long cstride;  // bytes between output rows c'
-    if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c') VB
-      base = gout + ((q * 32 + warp) * L + lane) * VB;
-      cstride = 32 * VB;
-    } else {
-      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * VB;
-      cstride = ((long long)VB << P) * 32;
-    }
-#pragma unroll
-    for (int j = 0; j < NG2; ++j)
-#pragma unroll
-      for (int c = 0; c < (1 << S1); ++c) {
-        const int v = (j << S1) + c;
-        uint32_t xr = re[v], xi = im[v];
-        if constexpr (SCALE_OUT) {  // conj + 1/n, one rounded mul each (fft.cpp:94-98)
-          if constexpr (A::kWords == 1) {
-            xr = A::mul(xr ^ 0x80000000u, p.scale);
-          } else {
-            xr = A::mul(xr, p.scale);
-            xi = A::mul(A::neg(xi), p.scale);
-          }
-        }
-        uint8_t* dst;
-        if constexpr (FIRST)
-          dst = base + ((long long)(j << S1) * L) * VB + c * cstride;
-        else
-          dst = base + (((long long)(j << S1) * VB) << P) + c * cstride;
+      for (int c = 0; c < 32; ++c) {
+        const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
         if constexpr (A::kWords == 1) {
-          if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
-          else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
+          re[c] = ptx::lds32(a);
+          if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
         } else {
-          if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
-          else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+          ptx::lds64(a, re[c], im[c]);
+          if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
         }
       }
+#pragma unroll
+      for (int pl = 0; pl < 5; ++pl) {
+        uint32_t nre[32], nim[32];
+#pragma unroll
+        for (int rl = 0; rl < (1 << pl); ++rl) {
+          const int slot1 = (1 << pl) - 1 + rl;
+          const uint4 tw = FIRST ? ptx::lds128(tw_base + slot1 * 16)
+                                 : ptx::lds128(tw_base + (slot1 * 32 + lane) * 16);
+#pragma unroll
+          for (int qq = 0; qq < (16 >> pl); ++qq) {
+            const int jl = (qq << pl) | rl;
+            const int oa = (qq << (pl + 1)) + rl;
+            butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa],
+                                   nim[oa], nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          re[x] = nre[x];
+          if constexpr (A::kWords == 2) im[x] = nim[x];
+        }
+      }
+      // ---- exchange through the padded slot: [col][local pos] ---------------
+      group_sync();  // every stage-1 read of the TMA tile is done
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
+        if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
+      }
+      group_sync();
+      // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
+      // column output), later groups lanes walk columns (contiguous rows)
+#pragma unroll
+      for (int j = 0; j < NG2; ++j) {
+        const int col = FIRST ? warp + (j << S1) : lane;
+        const int rl_ = FIRST ? lane : warp + (j << S1);
+#pragma unroll
+        for (int c = 0; c < (1 << S1); ++c) {
+          const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
+          const int v = (j << S1) + c;
+          if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
+        }
+      }
+      // release the slot to this group's tile S ahead
+      ptx::fence_proxy_async_smem();
+      group_sync();
+      if (leader && i + S < k) issue_load(q, rb, b + G * S, slot);
+      // ---- stage 2 ----------------------------------------------------------
+      const uint4* tw2 = FIRST ? nullptr
+                               : p.tw + (long long)rb * mp_block_records(S1) + 31 * 32 +
+                                     warp * 32 + lane;
+#pragma unroll
+      for (int pl = 0; pl < S1; ++pl) {
+        uint32_t nre[32], nim[32];
+#pragma unroll
+        for (int rl = 0; rl < (1 << pl); ++rl)
+#pragma unroll
+          for (int j = 0; j < NG2; ++j) {
+            const int slot2 = (1 << pl) - 1 + rl;
+            uint4 tw;
+            if constexpr (FIRST)
+              tw = ptx::lds128(tw_base + (31 + (slot2 << 5) + lane) * 16);
+            else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
+              tw = ptx::lds128(tw_base + (31 * 32 + (warp << 5) + lane +
+                                          (((slot2 << 5) + (j << S1)) << 5)) * 16);
+            else  // r_l = warp + 2^S1 j
+              tw = __ldg(tw2 + ((slot2 << 5) + (j << S1)) * 32);
+#pragma unroll
+            for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
+              const int jl = (qq << pl) | rl;
+              const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
+              const int oa = (j << S1) + (qq << (pl + 1)) + rl;
+              butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
+                                     nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
+            }
+          }
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+          re[x] = nre[x];
+          if constexpr (A::kWords == 2) im[x] = nim[x];
+        }
+      }
+      // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') ------------------------
+      uint8_t* gout = p.out + b * N * VB;
+      uint8_t* base;
+      long long cstride;  // bytes between output rows c'
+      if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c') VB
+        base = gout + ((q * 32 + warp) * L + lane) * VB;
+        cstride = 32 * VB;
+      } else {
+        base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * VB;
+        cstride = ((long long)VB << P) * 32;
+      }
+#pragma unroll
+      for (int j = 0; j < NG2; ++j)
+#pragma unroll
+        for (int c = 0; c < (1 << S1); ++c) {
+          const int v = (j << S1) + c;
+          uint32_t xr = re[v], xi = im[v];
+          if constexpr (SCALE_OUT) {  // conj + 1/n, one rounded mul each (fft.cpp:94-98)
+            if constexpr (A::kWords == 1) {
+              xr = A::mul(xr ^ 0x80000000u, p.scale);
+            } else {
+              xr = A::mul(xr, p.scale);
+              xi = A::mul(A::neg(xi), p.scale);
+            }
+          }
+          uint8_t* dst;
+          if constexpr (FIRST)
+            dst = base + ((long long)(j << S1) * L) * VB + c * cstride;
+          else
+            dst = base + (((long long)(j << S1) * VB) << P) + c * cstride;
+          if constexpr (A::kWords == 1) {
+            if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
+            else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
+          } else {
+            if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+            else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+          }
+        }
+    }
+    it += k;
   }
 }
 
@@ -411,19 +399,30 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
                         cudaStream_t st) {
   using Lay = MpLayout<S1, A>;
   MpParams q = p;
-  // ring depth; fp32 at s = 9 only fits a 1-deep ring (no prefetch, still correct)
-  const char* env = std::getenv("DSFFT_MP_STAGES");
-  int stages = env && *env ? std::max(1, std::atoi(env)) : 2;
-  while (stages > 1 && Lay::smem_bytes(first, stages) > smem_optin) --stages;
+  // ring depth S and tile groups per CTA G.  First groups (tiny twiddle
+  // table) run one group per CTA and several CTAs per SM; later groups share
+  // one column-block slab between G groups of one CTA (<= 512 threads).
+  const char* es = std::getenv("DSFFT_MP_STAGES");
+  const char* eg = std::getenv("DSFFT_MP_GROUPS");
+  int stages = es && *es ? std::max(1, std::atoi(es)) : 2;
+  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : (first ? 1 : std::max(1, 512 / Lay::T));
+  groups = std::min(groups, std::max(1, 512 / Lay::T));
+  while (groups > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --groups;
+  while (stages > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --stages;
   q.stages = stages;
-  const size_t smem = Lay::smem_bytes(first, stages);
-  const int per_sm = std::max(1, int(std::min<size_t>(smem_optin / smem, 2048 / Lay::T)));
-  const int grid = int(std::min<long long>(p.tiles, (long long)sm_count * per_sm));
+  const size_t smem = Lay::smem_bytes(first, stages, groups);
+  const int threads = groups * Lay::T;
+  const int regs = A::kWords == 1 ? 80 : 128;
+  const int per_sm = std::max(1, int(std::min<size_t>(
+                                     {smem_optin / smem, size_t(2048 / threads),
+                                      size_t(65536 / (threads * regs))})));
+  const int grid = int(std::min<long long>((p.tiles + groups - 1) / groups,
+                                           (long long)sm_count * per_sm));
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<grid, Lay::T, smem, st>>>(map, q);
+    kern<<<grid, threads, smem, st>>>(map, q);
     return cudaGetLastError();
   };
   if (first)  // never last: every split has >= 2 groups

@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -p no:cacheprovider -k "multipass or many_streams" > gpurun_out/pytest_mp.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_mp.log
+b() { local label=$1; shift
+  env $ENVS timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-accuracy "$@" > gpurun_out/b_$label.log 2>&1
+  echo "$label $ENVS: $(python -c "import json; d=json.loads(open('gpurun_out/b_$label.log').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],4), 'frac', round(d['roofline']['frac'],4), d['gpu_launches'])" 2>&1 | tail -1)"; }
+for n in 8192 65536 1048576 16777216; do ENVS="" b n${n} --n $n; ENVS="" b n${n}_f32 --n $n --precision fp32; done
+for gr in 1 2 4; do ENVS="DSFFT_MP_GROUPS=$gr" b n65536_g$gr --n 65536; ENVS="DSFFT_MP_GROUPS=$gr" b n8192_g$gr --n 8192; done
