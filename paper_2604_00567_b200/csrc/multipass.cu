@@ -135,18 +135,25 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   if (leader) pol = ptx::policy_evict_first();
   const int nb = int(p.nb);
   // TMA load of transform b of column block (q, rb) into ring slot `slot`
+  // (fp16 pairs: transforms b and b+1 land in the two halves of the slot; a
+  // b+1 past the batch is zero-filled by TMA and never stored)
+  constexpr int PAIR = A::kPair;
+  constexpr int EB = A::kSampleBytes;           // bytes of one complex in memory
+  constexpr int HALF = 32 * L * EB;             // one transform's tile
   auto issue_load = [&](long long q, int rb, int b, int slot) {
     uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
     ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
 #pragma unroll
-    for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
-      if constexpr (FIRST)
-        ptx::tma_load_3d(dst + size_t(r0) * 32 * VB, &in_map, int(q * 32), r0,
-                         int(b + p.b_off), &bars[slot], pol);
-      else
-        ptx::tma_load_4d(dst + size_t(r0) * 32 * VB, &in_map, rb * 32, int(q), r0,
-                         int(b + p.b_off), &bars[slot], pol);
-    }
+    for (int h = 0; h < PAIR; ++h)
+#pragma unroll
+      for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
+        if constexpr (FIRST)
+          ptx::tma_load_3d(dst + h * HALF + size_t(r0) * 32 * EB, &in_map, int(q * 32), r0,
+                           int(b + h + p.b_off), &bars[slot], pol);
+        else
+          ptx::tma_load_4d(dst + h * HALF + size_t(r0) * 32 * EB, &in_map, rb * 32, int(q), r0,
+                           int(b + h + p.b_off), &bars[slot], pol);
+      }
   };
 
   long long it = 0;  // this group's running tile count (ring slot / phase)
@@ -164,11 +171,14 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
       for (int i = threadIdx.x; i < Lay::kSlabRecords; i += blockDim.x) tws[i] = src[i];
       __syncthreads();
     }
-    const int k = b1 - b0 > g ? (b1 - b0 - g + G - 1) / G : 0;  // this group's tiles
+    const int units = (b1 - b0 + PAIR - 1) / PAIR;  // tiles (transform pairs for fp16)
+    const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
     if (leader)
-      for (int i = 0; i < S && i < k; ++i) issue_load(q, rb, b0 + g + G * i, int((it + i) % S));
+      for (int i = 0; i < S && i < k; ++i)
+        issue_load(q, rb, b0 + PAIR * (g + G * i), int((it + i) % S));
     for (int i = 0; i < k; ++i) {
-      const int b = b0 + g + G * i;
+      const int b = b0 + PAIR * (g + G * i);
+      const bool second = PAIR == 2 && b + 1 < b1;  // pair partner exists in this unit
       const int slot = int((it + i) % S);
       const uint32_t buf = ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes);
       ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
@@ -178,7 +188,13 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
-        if constexpr (A::kWords == 1) {
+        if constexpr (PAIR == 2) {  // (re0,re1), (im0,im1) from the two halves
+          const uint32_t e = buf + (((warp + (c << S1)) << 5) + lane) * EB;
+          const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
+          re[c] = __byte_perm(lo, hi, 0x5410);
+          im[c] = __byte_perm(lo, hi, 0x7632);
+          if constexpr (CONJ_IN) im[c] = A::neg(im[c]);  // conj on load (fft.cpp:90-91)
+        } else if constexpr (A::kWords == 1) {
           re[c] = ptx::lds32(a);
           if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
         } else {
@@ -232,7 +248,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
       // release the slot to this group's tile S ahead
       ptx::fence_proxy_async_smem();
       group_sync();
-      if (leader && i + S < k) issue_load(q, rb, b + G * S, slot);
+      if (leader && i + S < k) issue_load(q, rb, b + PAIR * G * S, slot);
       // ---- stage 2 ----------------------------------------------------------
       const uint4* tw2 = FIRST ? nullptr
                                : p.tw + (long long)rb * mp_block_records(S1) + 31 * 32 +
@@ -269,15 +285,16 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
         }
       }
       // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') ------------------------
-      uint8_t* gout = p.out + b * N * VB;
+      // element offsets in units of one stored complex (EB bytes)
+      uint8_t* gout = p.out + b * N * EB;
       uint8_t* base;
       long long cstride;  // bytes between output rows c'
-      if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c') VB
-        base = gout + ((q * 32 + warp) * L + lane) * VB;
-        cstride = 32 * VB;
+      if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
+        base = gout + ((q * 32 + warp) * L + lane) * EB;
+        cstride = 32 * EB;
       } else {
-        base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * VB;
-        cstride = ((long long)VB << P) * 32;
+        base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * EB;
+        cstride = ((long long)EB << P) * 32;
       }
 #pragma unroll
       for (int j = 0; j < NG2; ++j)
@@ -295,10 +312,21 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
           }
           uint8_t* dst;
           if constexpr (FIRST)
-            dst = base + ((long long)(j << S1) * L) * VB + c * cstride;
+            dst = base + ((long long)(j << S1) * L) * EB + c * cstride;
           else
-            dst = base + (((long long)(j << S1) * VB) << P) + c * cstride;
-          if constexpr (A::kWords == 1) {
+            dst = base + (((long long)(j << S1) * EB) << P) + c * cstride;
+          if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
+            unsigned int* d0 = reinterpret_cast<unsigned int*>(dst);
+            unsigned int* d1 = reinterpret_cast<unsigned int*>(dst + N * EB);
+            const uint32_t t0 = __byte_perm(xr, xi, 0x5410), t1 = __byte_perm(xr, xi, 0x7632);
+            if constexpr (LAST) {
+              __stcs(d0, t0);
+              if (second) __stcs(d1, t1);
+            } else {
+              __stcg(d0, t0);
+              if (second) __stcg(d1, t1);
+            }
+          } else if constexpr (A::kWords == 1) {
             if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
             else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
           } else {
@@ -325,6 +353,7 @@ struct MpGroup {
 
 struct MultipassPlan {
   int m = 0, strategy = 0, precision = 0, sm_count = 0;
+  bool f16_pairs = true;  // fp16 value layout: transform pairs (else one complex/register)
   size_t smem_optin = 0;
   std::vector<MpGroup> groups;
   size_t chunk_transforms = 0;
@@ -461,7 +490,11 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   mp->precision = precision;
   mp->sm_count = sm_count;
   mp->smem_optin = smem_optin;
-  const bool f16c = precision == kFp16;  // one complex per f16x2 register
+  // fp16: transform pairs share every twiddle record and per-tile overhead
+  // between two transforms (DSFFT_MP_F16_LAYOUT=2 selects one complex/register)
+  const char* lay = std::getenv("DSFFT_MP_F16_LAYOUT");
+  mp->f16_pairs = !(lay && std::atoi(lay) == 2);
+  const bool f16c = precision == kFp16 && !mp->f16_pairs;
   auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
   int P = 0;
   for (int s : split_passes(m, 9)) {
@@ -579,19 +612,19 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       p.scale = scale;
       const bool first = i == 0, last = i == ng - 1;
       const int S1 = g.s - 5;
-      cudaError_t e =
-          f16 ? (std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, first && inverse,
-                                                     last && inverse, last, mp.sm_count,
-                                                     mp.smem_optin, stream)
-                      : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, first && inverse,
-                                                      last && inverse, last, mp.sm_count,
-                                                      mp.smem_optin, stream))
-              : (std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, first && inverse,
-                                                    last && inverse, last, mp.sm_count,
-                                                    mp.smem_optin, stream)
-                      : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, first && inverse,
-                                                     last && inverse, last, mp.sm_count,
-                                                     mp.smem_optin, stream));
+      const bool ci = first && inverse, so = last && inverse;
+      const int sm = mp.sm_count;
+      const size_t oi = mp.smem_optin;
+      cudaError_t e;
+      if (f16 && mp.f16_pairs)
+        e = std_ ? mp_launch_a<ArithF16P, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
+                 : mp_launch_a<ArithF16P, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
+      else if (f16)
+        e = std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
+                 : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
+      else
+        e = std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
+                 : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
       if (e != cudaSuccess) {
         g_mp_err = std::string("mp_kernel launch: ") + cudaGetErrorString(e);
         return 1;
