@@ -293,6 +293,18 @@ def main():
         acc = {"max_rel_l2_vs_fp64": rep["rel_l2_max"], "median_rel_l2": rep["rel_l2_median"],
                "nonfinite": rep["nonfinite_trials"], "transforms": rep["trials"],
                "how": "dsfft_error_device over the whole batch (FP64 reference transform)"}
+        # the paper's claim on the same batch: dual-select within Eq. 11's bound
+        # and below Linzer-Feig-with-clamp (north_star; analysis.cpp:61-63)
+        if args.strategy == "dual" and prec in ("fp16", "fp32"):
+            eps = 2.0 ** -11 if prec == "fp16" else 2.0 ** -24
+            tab = dsfft.build_table(n, "dual", "fp64")
+            acc["paper_bound"] = (1.0 + float(np.abs(tab["ratio"]).max()) * eps) ** \
+                int(np.log2(n)) - 1.0
+            lf = dsfft.error_device(dsfft.make_plan(n, "lf", prec, device=local_dev), x,
+                                    "forward")
+            acc["lf_max"], acc["lf_median"] = lf["rel_l2_max"], lf["rel_l2_median"]
+            acc["dual_beats_lf"] = rep["rel_l2_median"] < lf["rel_l2_median"]
+            acc["within_bound"] = rep["rel_l2_max"] <= acc["paper_bound"]
         # host cross-check on a few transforms: numpy FP64 FFT
         idx = torch.arange(0, batch, max(1, batch // 16), device=dev)[:16]
         acc["numpy_check_max"], _ = accuracy_sample(y[idx].cpu().numpy(), x[idx].cpu().numpy(),

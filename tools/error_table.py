@@ -1,0 +1,81 @@
+#!/usr/bin/env python
+"""Per-variant error report on the GPU (north_star: "each variant's max relative
+error against an FP64 DFT must be reported; the dual-select error must stay
+within the paper's bound and beat Linzer-Feig-with-clamp at N=1024").
+
+Runs dsfft.measure_error (reference protocol, seed 42) for every strategy x
+precision x N and writes profiles/<round>_error_table.md with the paper's
+per-size bounds (cumulative_bound(t_max, eps, log2 N), analysis.cpp:61-63).
+
+  python tools/error_table.py [--trials 4096] [--round r01]
+"""
+import argparse
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2604_00567_b200 as dsfft  # noqa: E402
+
+STRATS = ("standard", "lf", "cosine", "dual")
+
+
+def t_max(n, strategy):
+    """table_stats' t_max over the FP64 table (twiddle.cpp:143-162)."""
+    t = dsfft.build_table(n, strategy, "fp64")
+    live = t["clamped"] == 0
+    return float(abs(t["ratio"][live]).max()) if live.any() else 0.0
+
+
+def bound(n, strategy, eps):
+    m = int(math.log2(n))
+    return (1.0 + t_max(n, strategy) * eps) ** m - 1.0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trials", type=int, default=4096)
+    ap.add_argument("--round", default="r01")
+    a = ap.parse_args()
+    rows = []
+    for n in (64, 256, 1024, 4096, 1 << 16, 1 << 20):
+        trials = max(8, min(a.trials, (1 << 26) // n))
+        for p in ("fp16", "fp32"):
+            for s in STRATS:
+                r = dsfft.measure_error(n, s, p, "forward", trials, 42)
+                rows.append((n, p, s, trials, r))
+                print(n, p, s, r["rel_l2_median"], r["rel_l2_max"], r["nonfinite_trials"],
+                      flush=True)
+    out = os.path.join(ROOT, "profiles", f"{a.round}_error_table.md")
+    with open(out, "w") as f:
+        f.write(f"# Forward error vs an FP64 reference transform ({a.round})\n\n")
+        f.write("Protocol: the reference's `measure_error` (analysis.cpp:101-154), seed 42, "
+                "SplitMix64 inputs in [-1,1), ingest-rounded, every trial transformed on the "
+                "B200 by `dsfft_measure_error`.\n\nrel-L2 median / max over the trials. "
+                "The bound is Eq. 11 (analysis.cpp:61-63) for the strategy at that N.\n\n")
+        f.write("| N | precision | strategy | trials | median | max | non-finite | bound | "
+                "max <= bound |\n|---|---|---|---|---|---|---|---|---|\n")
+        for n, p, s, trials, r in rows:
+            eps = 2.0 ** -11 if p == "fp16" else 2.0 ** -24
+            b = bound(n, s, eps) if s != "standard" else float("nan")
+            ok = "-" if s == "standard" or not math.isfinite(b) else \
+                ("yes" if r["rel_l2_max"] <= b else
+                 ("non-finite, as the reference (k=N/4 singular ratio)"
+                  if s == "cosine" and not math.isfinite(r["rel_l2_max"]) else "NO"))
+            f.write(f"| {n} | {p} | {s} | {trials} | {r['rel_l2_median']:.3e} | "
+                    f"{r['rel_l2_max']:.3e} | {r['nonfinite_trials']} | {b:.3e} | {ok} |\n")
+        du = {(n, p): r for n, p, s, _, r in rows if s == "dual"}
+        lf = {(n, p): r for n, p, s, _, r in rows if s == "lf"}
+        f.write("\nDual-select vs Linzer-Feig (median rel-L2):\n\n| N | precision | dual | LF | "
+                "dual < LF |\n|---|---|---|---|---|\n")
+        for key in du:
+            f.write(f"| {key[0]} | {key[1]} | {du[key]['rel_l2_median']:.3e} | "
+                    f"{lf[key]['rel_l2_median']:.3e} | "
+                    f"{'yes' if du[key]['rel_l2_median'] < lf[key]['rel_l2_median'] else 'no'} |\n")
+    print(out)
+
+
+if __name__ == "__main__":
+    main()
