@@ -23,7 +23,7 @@ using CfgW = Sched<7, 5, 1, 4, 3>;
 using CfgC = Sched<7, 5, 1, 1, 5, 1>;
 #elif DSFFT_M == 8
 using CfgW = Sched<8, 5, 1, 4, 4>;
-using CfgC = CfgW;
+using CfgC = Sched<8, 5, 1, 1, 5, 2>;  // conflict-free for 4-byte values
 #elif DSFFT_M == 9
 using CfgW = Sched<9, 5, 1, 5, 4>;
 using CfgC = CfgW;
