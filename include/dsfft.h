@@ -87,6 +87,15 @@ int dsfft_plan_info(dsfft_plan plan, size_t* n, unsigned* m, int* strategy, int*
 int dsfft_build_table(size_t n, int strategy, int precision, double clamp_eps, dsfft_entry* out,
                       size_t count);
 
+/* The table dump in the reference's CSV schema, write_table_csv
+ * (serialize.cpp:48-57: "k,theta,omega_r,omega_i,path,multiplier,ratio,clamped",
+ * %.17g): precision fp64 gives the CLI `twiddles` dump of build_table
+ * (main.cpp:34-42); fp16/fp32 give the plan's rounded table, i.e. exactly the
+ * values the device records are packed from.  Returns the bytes needed
+ * including the terminating NUL (0 on error); copies when `cap` suffices. */
+size_t dsfft_table_csv(size_t n, int strategy, int precision, double clamp_eps, char* out,
+                       size_t cap);
+
 /* Copy of the plan's rounded table: FftPlan::table.entries (n/2 records). */
 int dsfft_plan_table(dsfft_plan plan, dsfft_entry* out, size_t count);
 

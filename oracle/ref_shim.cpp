@@ -229,3 +229,30 @@ int ref_table_stats(std::size_t n, int s, double* t_max, uint64_t* argmax_k,
 }
 
 }  // extern "C"
+
+#ifdef REF_HAVE_SERIALIZE
+#include <sstream>
+
+#include "fmafft/serialize.hpp"
+
+extern "C" {
+// write_table_csv (serialize.cpp:48-57) of build_table (the CLI `twiddles`
+// dump, main.cpp:34-42) or, for precision fp16/fp32, of make_plan's rounded
+// table.  Returns the bytes needed (incl. NUL); copies when cap suffices.
+size_t ref_table_csv(std::size_t n, int s, int p, double clamp_eps, char* out, size_t cap) {
+  std::ostringstream os;
+  try {
+    if (p == 2)
+      fmafft::write_table_csv(os, fmafft::build_table(n, S(s), clamp_eps));
+    else
+      fmafft::write_table_csv(os, fmafft::make_plan(n, S(s), P(p)).table);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 0;
+  }
+  const std::string str = os.str();
+  if (out && cap > str.size()) std::memcpy(out, str.c_str(), str.size() + 1);
+  return str.size() + 1;
+}
+}
+#endif

@@ -159,6 +159,23 @@ def make_plan(n: int, strategy: str = "dual", precision: str = "fp32",
     return FftPlan(int(n), m, strategy, precision, device, h)
 
 
+def table_csv(n: int, strategy: str, precision: str = "fp64", clamp_eps: float = 1e-7) -> str:
+    """write_table_csv (serialize.cpp:48-57) of build_table (fp64, the CLI
+    `twiddles` dump) or of the plan's rounded table (fp16 / fp32)."""
+    lib = _load()
+    lib.dsfft_table_csv.restype = C.c_size_t
+    lib.dsfft_table_csv.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_double, C.c_char_p,
+                                    C.c_size_t]
+    args = (int(n), STRATEGIES[parse_strategy(strategy)], PRECISIONS[parse_precision(precision)],
+            float(clamp_eps))
+    need = lib.dsfft_table_csv(*args, None, 0)
+    if need == 0:
+        raise ValueError(lib.dsfft_last_error().decode())
+    buf = C.create_string_buffer(need)
+    lib.dsfft_table_csv(*args, buf, need)
+    return buf.value.decode()
+
+
 def build_table(n: int, strategy: str, precision: str = "fp64",
                 clamp_eps: float = 1e-7) -> np.ndarray:
     """Host table builder: make_plan's rounded table (fp64: build_table)."""

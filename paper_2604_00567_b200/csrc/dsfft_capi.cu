@@ -383,6 +383,40 @@ int dsfft_build_table(size_t n, int strategy, int precision, double clamp_eps, d
   return DSFFT_OK;
 }
 
+size_t dsfft_table_csv(size_t n, int strategy, int precision, double clamp_eps, char* out,
+                       size_t cap) {
+  std::vector<dsfft::TableEntry> t;
+  try {
+    t = dsfft::plan_table(n, strategy, precision, clamp_eps);
+  } catch (const std::exception& e) {
+    fail(DSFFT_ERR_INVALID, e.what());
+    return 0;
+  }
+  std::string s = "k,theta,omega_r,omega_i,path,multiplier,ratio,clamped\n";
+  char buf[48];
+  auto num = [&](double v) {  // format_double: %.17g (serialize.cpp:42-46)
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    s += buf;
+  };
+  for (size_t k = 0; k < t.size(); ++k) {
+    const auto& e = t[k];
+    s += std::to_string(k);
+    s += ',';
+    num(dsfft::twiddle_angle(k, n));
+    s += ',';
+    num(e.omega_r);
+    s += ',';
+    num(e.omega_i);
+    s += e.path == dsfft::kCos ? ",COS," : ",SIN,";
+    num(e.multiplier);
+    s += ',';
+    num(e.ratio);
+    s += e.clamped ? ",true\n" : ",false\n";
+  }
+  if (out && cap > s.size()) std::memcpy(out, s.c_str(), s.size() + 1);
+  return s.size() + 1;
+}
+
 int dsfft_plan_table(dsfft_plan p, dsfft_entry* out, size_t count) {
   if (!p || !out) return fail(DSFFT_ERR_INVALID, "null argument");
   if (count < p->table.size()) return fail(DSFFT_ERR_INVALID, "output too small");

@@ -68,6 +68,20 @@ def main():
         stats.append([st["t_max"], st["argmax_k"], st["singular_count"], st["cos_path_count"],
                       st["sin_path_count"]])
     out["table_stats/1024/lf_cosine_dual"] = np.array(stats, dtype=np.float64)
+    # write_table_csv (serialize.cpp:48-57), when the reference's serializer
+    # was built (oracle/Makefile links it if nlohmann/json.hpp is available)
+    import ctypes as C
+    lib = ref.lib
+    if hasattr(lib, "ref_table_csv"):
+        lib.ref_table_csv.restype = C.c_size_t
+        lib.ref_table_csv.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_double, C.c_char_p,
+                                      C.c_size_t]
+        for n, s, p in ((64, 3, 2), (64, 1, 2), (1024, 3, 0), (256, 2, 1), (8, 0, 2)):
+            need = lib.ref_table_csv(n, s, p, 1e-7, None, 0)
+            buf = C.create_string_buffer(need)
+            lib.ref_table_csv(n, s, p, 1e-7, buf, need)
+            out[f"csv/{n}/{STRATS[s]}/{('fp16', 'fp32', 'fp64')[p]}"] = \
+                np.frombuffer(buf.value, dtype=np.uint8)
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes,", len(out), "arrays")

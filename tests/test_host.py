@@ -57,6 +57,19 @@ def test_host_tables_match_reference(dsfft, ref):
                 assert dsfft.build_table(n, s, p).tobytes() == ref.plan_table(n, s, p).tobytes()
 
 
+def test_table_csv_matches_reference_writer(dsfft):
+    """dsfft_table_csv == the reference's write_table_csv (serialize.cpp:48-57),
+    byte for byte (golden dumps produced by the reference's own serializer)."""
+    g = np.load(GOLDEN)
+    keys = [k for k in g.files if k.startswith("csv/")]
+    assert len(keys) >= 5
+    for key in keys:
+        _, n, s, p = key.split("/")
+        assert dsfft.table_csv(int(n), s, p).encode() == g[key].tobytes(), key
+    with pytest.raises(ValueError, match="power of two"):
+        dsfft.table_csv(12, "dual")
+
+
 def test_ingest_rounding_matches_oracle(dsfft, orc):
     rng = np.random.RandomState(916)
     x = (1 + rng.randint(0, 1 << 52, 300000) * 2.0 ** -52) * np.exp2(rng.randint(-30, 21, 300000))
