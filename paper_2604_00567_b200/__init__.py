@@ -27,7 +27,8 @@ __all__ = ["Strategy", "Precision", "FftPlan", "make_plan", "forward", "inverse"
            "parse_strategy", "parse_precision", "library_path", "DsfftError"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libdsfft.so")
+# DSFFT_LIBRARY: load another build of the library (A/B timing of two builds)
+_LIB_PATH = os.environ.get("DSFFT_LIBRARY") or os.path.join(_PKG, "libdsfft.so")
 
 # fmafft::Strategy / Precision declaration order (twiddle.hpp:14, precision.hpp:12)
 STRATEGIES = {"standard": 0, "lf": 1, "cosine": 2, "dual": 3}

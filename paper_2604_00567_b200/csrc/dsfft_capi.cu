@@ -144,6 +144,9 @@ void choose_small_launch(dsfft_plan_s* p, int default_stages) {
   int want = env_int("DSFFT_GROUPS", 0);
   int groups = 0;
   for (int ng = max_groups; ng >= 1; --ng) {
+    // whole warps per SM sub-partition: 13 one-warp groups leave one SMSP
+    // with 4 warps and three with 3 (measured -20% at N=1024 vs 12)
+    if (ng * g.warps > 4 && (ng * g.warps) % 4 != 0) continue;
     if (p->small->smem_bytes(ng, stages) <= p->smem_optin) {
       groups = ng;
       break;
@@ -174,9 +177,10 @@ int upload_small_tables(dsfft_plan_s* p) {
                                          p->variant == dsfft::kVarF16C);
         }
   }
-  DSFFT_CUDA(cudaMalloc(&p->d_tw, rec.size() * sizeof(dsfft::Record)));
-  DSFFT_CUDA(cudaMemcpy(p->d_tw, rec.data(), rec.size() * sizeof(dsfft::Record),
-                        cudaMemcpyHostToDevice));
+  const std::vector<uint8_t> img = dsfft::serialize_records(
+      rec, dsfft::record_bytes(p->precision, p->variant == dsfft::kVarF16C));
+  DSFFT_CUDA(cudaMalloc(&p->d_tw, img.size()));
+  DSFFT_CUDA(cudaMemcpy(p->d_tw, img.data(), img.size(), cudaMemcpyHostToDevice));
   return DSFFT_OK;
 }
 

@@ -67,16 +67,17 @@ struct F16Ops {
 
 // FP16, transform pairs: two words per value, two real transforms per
 // virtual transform.
+// Records are 8 bytes, (t | w' << 16, sel | w << 16), expanded by load_rec.
 struct ArithF16P : F16Ops {
-  static constexpr int kWords = 2, kPair = 2, kSampleBytes = 4;
+  static constexpr int kWords = 2, kPair = 2, kSampleBytes = 4, kRecBytes = 8;
 };
 // FP16, one complex per register.
 struct ArithF16C : F16Ops {
-  static constexpr int kWords = 1, kPair = 1, kSampleBytes = 4;
+  static constexpr int kWords = 1, kPair = 1, kSampleBytes = 4, kRecBytes = 16;
 };
 
 struct ArithF32 {
-  static constexpr int kWords = 2, kPair = 1, kSampleBytes = 8;
+  static constexpr int kWords = 2, kPair = 1, kSampleBytes = 8, kRecBytes = 16;
   __device__ __forceinline__ static float f(uint32_t a) { return __uint_as_float(a); }
   __device__ __forceinline__ static uint32_t u(float a) { return __float_as_uint(a); }
   __device__ __forceinline__ static uint32_t fma(uint32_t a, uint32_t b, uint32_t c) {
@@ -87,6 +88,34 @@ struct ArithF32 {
   __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) { return u(__fsub_rn(f(a), f(b))); }
   __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) { return u(__fmul_rn(f(a), f(b))); }
 };
+
+// A twiddle record from shared memory (byte address a) in the 4-word form the
+// butterflies use; compact fp16 pair records expand to ((t,t), (w',w'), (w,w),
+// sel) -- the broadcasts fold into the HFMA2 operands.
+template <class A>
+__device__ __forceinline__ uint4 expand_rec(uint32_t x, uint32_t y) {
+  return make_uint4(ptx::bcast_lo(x), ptx::bcast_hi(x), ptx::bcast_hi(y), y);
+}
+template <class A>
+__device__ __forceinline__ uint4 load_rec(uint32_t a) {
+  if constexpr (A::kRecBytes == 8) {
+    uint32_t x, y;
+    ptx::lds64(a, x, y);
+    return expand_rec<A>(x, y);
+  } else {
+    return ptx::lds128(a);
+  }
+}
+// Same from global memory (read-only path).
+template <class A>
+__device__ __forceinline__ uint4 ldg_rec(const uint8_t* p) {
+  if constexpr (A::kRecBytes == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    return expand_rec<A>(v.x, v.y);
+  } else {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  }
+}
 
 // Bytes of one stored value (one complex or one transform-pair sample).
 template <class A>
@@ -156,18 +185,19 @@ __device__ __forceinline__ void run_stage(uint32_t (&re)[Cfg::E], uint32_t (&im)
   constexpr int m = Cfg::LOG_N, s = Cfg::s(ST), P = Cfg::P(ST);
   constexpr int E = Cfg::E, NGRP = E >> s, H = 1 << (s - 1);
   constexpr bool kSharedR = (Cfg::T % (1 << P)) == 0;  // r independent of j
-  const uint32_t tws = tw_base + Cfg::tw_off(ST) * 16;
+  constexpr int RB = A::kRecBytes;
+  const uint32_t tws = tw_base + Cfg::tw_off(ST) * RB;
 #pragma unroll
   for (int pl = 0; pl < s; ++pl) {
     uint32_t nre[E], nim[E];
 #pragma unroll
     for (int rl = 0; rl < (1 << pl); ++rl) {
       uint4 tw{};
-      if constexpr (kSharedR) tw = ptx::lds128(tws + tw_slot(P, grp_r(m, P, s, t), pl, rl) * 16);
+      if constexpr (kSharedR) tw = load_rec<A>(tws + tw_slot(P, grp_r(m, P, s, t), pl, rl) * RB);
 #pragma unroll
       for (int j = 0; j < NGRP; ++j) {
         if constexpr (!kSharedR)
-          tw = ptx::lds128(tws + tw_slot(P, grp_r(m, P, s, t + Cfg::T * j), pl, rl) * 16);
+          tw = load_rec<A>(tws + tw_slot(P, grp_r(m, P, s, t + Cfg::T * j), pl, rl) * RB);
 #pragma unroll
         for (int q = 0; q < (H >> pl); ++q) {
           const int jl = (q << pl) | rl;
@@ -320,7 +350,7 @@ template <class Cfg, class A>
 struct SmallLayout {
   static constexpr int kBufBytes = Cfg::BUF_VALS * value_bytes<A>();
   static constexpr int kItemBytes = Cfg::VALS * value_bytes<A>();
-  static constexpr int kTwBytes = Cfg::TW_RECORDS * 16;
+  static constexpr int kTwBytes = (Cfg::TW_RECORDS * A::kRecBytes + 127) & ~127;
   static constexpr int kTpi = Cfg::K * A::kPair;            // real transforms per item
   static constexpr int kTb = Cfg::N * A::kSampleBytes;      // bytes per transform
   static size_t smem_bytes(int groups, int stages) {
@@ -343,7 +373,7 @@ __global__ void __launch_bounds__(max_threads<Cfg, A>(), 1) fft_small_kernel(con
                                                size_t(ng) * S * Lay::kBufBytes) +
                    gid * S;
   // twiddle records -> smem (once per persistent CTA)
-  for (int i = threadIdx.x; i < Cfg::TW_RECORDS; i += blockDim.x)
+  for (int i = threadIdx.x; i < (Cfg::TW_RECORDS * A::kRecBytes + 15) / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = p.tw[i];
   if (t == 0)
     for (int b = 0; b < S; ++b) ptx::mbar_init(&bars[b], 1);

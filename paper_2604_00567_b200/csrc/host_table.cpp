@@ -29,7 +29,6 @@ uint32_t f32_bits(double x) {
   return b;
 }
 
-uint32_t dup16(uint16_t h) { return uint32_t(h) | (uint32_t(h) << 16); }
 
 }  // namespace
 
@@ -180,11 +179,26 @@ Record pack_record(const TableEntry& e, int strategy, int precision, bool f16_co
     return Record{pair(-t, t), pair(cos ? w : -w, w), cos ? 0x3210u : 0x1032u,
                   cos ? 0x1032u : 0x3210u};
   }
-  auto word = [&](double v) -> uint32_t {
-    return precision == kFp16 ? dup16(half_bits(v)) : f32_bits(v);
-  };
-  if (strategy == kStandard) return Record{word(e.omega_r), word(e.omega_i), 0u, 0u};
-  return Record{word(t), word(cos ? w : -w), word(w), cos ? 0x3210u : 0x7654u};
+  if (precision == kFp16) {  // transform pairs: compact, halves broadcast on device
+    auto pair = [](uint32_t lo, double hi) -> uint32_t {
+      return lo | (uint32_t(half_bits(hi)) << 16);
+    };
+    if (strategy == kStandard) return Record{pair(half_bits(e.omega_r), e.omega_i), 0u, 0u, 0u};
+    return Record{pair(half_bits(t), cos ? w : -w), pair(cos ? 0x3210u : 0x7654u, w), 0u, 0u};
+  }
+  if (strategy == kStandard) return Record{f32_bits(e.omega_r), f32_bits(e.omega_i), 0u, 0u};
+  return Record{f32_bits(t), f32_bits(cos ? w : -w), f32_bits(w), cos ? 0x3210u : 0x7654u};
+}
+
+int record_bytes(int precision, bool f16_complex) {
+  return precision == kFp16 && !f16_complex ? 8 : 16;
+}
+
+std::vector<uint8_t> serialize_records(const std::vector<Record>& recs, int rec_bytes) {
+  std::vector<uint8_t> out((recs.size() * rec_bytes + 15) & ~size_t(15), 0);
+  for (size_t i = 0; i < recs.size(); ++i)
+    std::memcpy(out.data() + i * rec_bytes, &recs[i], rec_bytes);
+  return out;
 }
 
 }  // namespace dsfft

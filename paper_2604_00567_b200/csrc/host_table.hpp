@@ -49,15 +49,23 @@ uint16_t half_bits(double x);
 double half_value(uint16_t h);
 double round_to(double x, int precision);
 
-// 16-byte device twiddle record (see fft_kernels.cuh):
+// Device twiddle record (see fft_kernels.cuh), 16 bytes:
 //   FMA strategies: (t, w' = COS ? w : -w, w, PRMT selector)
 //   standard:       (omega_r, omega_i, 0, 0)
-// fp32 words hold binary32 bits; fp16 words hold the value twice (f16x2).
+// fp32 words hold binary32 bits.  fp16 transform pairs use 8 bytes,
+//   x = (t | w' << 16), y = (selector | w << 16)   (standard: x = (omega_r | omega_i << 16))
+// and the kernel broadcasts each half into both f16x2 lanes (folded into the
+// HFMA2 operand selects .H0_H0 / .H1_H1, no extra instructions).  fp16 one
+// complex per register: see pack_record.
 struct Record {
   uint32_t x, y, z, w;
 };
 Record pack_record(const TableEntry& rounded, int strategy, int precision,
                    bool f16_complex = false);
+// Bytes per device record for a precision / fp16 layout (8 or 16).
+int record_bytes(int precision, bool f16_complex);
+// Records -> device byte image (record_bytes each, padded to 16 bytes).
+std::vector<uint8_t> serialize_records(const std::vector<Record>& recs, int rec_bytes);
 
 // Effective (t, w, cos?) a butterfly uses for an entry: mirrors the operand
 // choice of butterfly_linzer_feig / butterfly_cosine / butterfly_dual

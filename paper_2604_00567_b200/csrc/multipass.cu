@@ -79,7 +79,7 @@ struct MpLayout {
   static constexpr bool kFullSlab = S1 <= 3;
   static constexpr int kSlabRecords = kFullSlab ? mp_block_records(S1) : 31 * 32;
   __host__ __device__ static constexpr int tw_bytes(bool first) {
-    return ((first ? mp_first_records(S1) * 16 : kSlabRecords * 16) + 127) & ~127;
+    return ((first ? mp_first_records(S1) : kSlabRecords) * A::kRecBytes + 127) & ~127;
   }
   static size_t smem_bytes(bool first, int stages, int groups) {
     const int tw = tw_bytes(first);
@@ -94,7 +94,8 @@ struct MpLayout {
 // later pass groups stage the unit's twiddle slab once, shared by all groups,
 // and group g takes transforms b0+g, b0+g+G, ... of the unit with its own TMA
 // ring.  Register budget: one-word values ~80, two-word ~128.
-template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST>
+template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST,
+          bool BOUT>
 __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     mp_kernel(const __grid_constant__ CUtensorMap in_map, const MpParams p) {
   using Lay = MpLayout<S1, A>;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   const int P = p.P;
   const long long N = 1LL << p.m;
   constexpr int tw_bytes = Lay::tw_bytes(FIRST);
+  constexpr int RB = A::kRecBytes;  // bytes per twiddle record
   uint4* tws = reinterpret_cast<uint4*>(smem);
   const uint32_t tw_base = ptx::smem_u32(smem);
   uint8_t* bufs = smem + tw_bytes + size_t(g) * S * Lay::kBufBytes;
@@ -121,16 +123,14 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   };
 
   if constexpr (FIRST) {  // column-independent twiddles: stage once per CTA
-    for (int i = threadIdx.x; i < mp_first_records(S1); i += blockDim.x) tws[i] = p.tw[i];
+    for (int i = threadIdx.x; i < (mp_first_records(S1) * RB + 15) / 16; i += blockDim.x)
+      tws[i] = p.tw[i];
   }
   if (leader)
     for (int i = 0; i < S; ++i) ptx::mbar_init(&bars[i], 1);
   ptx::fence_mbar_init();
   __syncthreads();
 
-  const long long per = (p.tiles + gridDim.x - 1) / gridDim.x;
-  const long long t_begin = blockIdx.x * per;
-  const long long t_end = t_begin + per < p.tiles ? t_begin + per : p.tiles;
   uint64_t pol = 0;
   if (leader) pol = ptx::policy_evict_first();
   const int nb = int(p.nb);
@@ -147,195 +147,252 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     for (int h = 0; h < PAIR; ++h)
 #pragma unroll
       for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
+        uint8_t* d = dst + h * HALF + size_t(r0) * 32 * EB;
+        const int bb = int(b + h + p.b_off);
         if constexpr (FIRST)
-          ptx::tma_load_3d(dst + h * HALF + size_t(r0) * 32 * EB, &in_map, int(q * 32), r0,
-                           int(b + h + p.b_off), &bars[slot], pol);
+          ptx::tma_load_3d(d, &in_map, int(q * 32), r0, bb, &bars[slot], pol);
+        else if constexpr (LAST)  // blocked intermediate {r_l, c, rb, b}
+          ptx::tma_load_4d(d, &in_map, 0, r0, rb, bb, &bars[slot], pol);
         else
-          ptx::tma_load_4d(dst + h * HALF + size_t(r0) * 32 * EB, &in_map, rb * 32, int(q), r0,
-                           int(b + h + p.b_off), &bars[slot], pol);
+          ptx::tma_load_4d(d, &in_map, rb * 32, int(q), r0, bb, &bars[slot], pol);
       }
   };
 
-  long long it = 0;  // this group's running tile count (ring slot / phase)
-  for (long long u0 = t_begin; u0 < t_end;) {
-    const long long tt = u0 / nb;  // column block of this unit
-    const int b0 = int(u0 - tt * nb);
-    const long long u1 = (tt + 1) * nb < t_end ? (tt + 1) * nb : t_end;
-    const int b1 = b0 + int(u1 - u0);
-    u0 = u1;
-    const long long q = FIRST ? tt : tt / rblocks;
-    const int rb = FIRST ? 0 : int(tt - q * rblocks);
-    if constexpr (!FIRST) {  // the unit's twiddle slab, shared by every group
-      __syncthreads();
-      const uint4* src = p.tw + (long long)rb * mp_block_records(S1);
-      for (int i = threadIdx.x; i < Lay::kSlabRecords; i += blockDim.x) tws[i] = src[i];
-      __syncthreads();
-    }
-    const int units = (b1 - b0 + PAIR - 1) / PAIR;  // tiles (transform pairs for fp16)
-    const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
-    if (leader)
-      for (int i = 0; i < S && i < k; ++i)
-        issue_load(q, rb, b0 + PAIR * (g + G * i), int((it + i) % S));
-    for (int i = 0; i < k; ++i) {
-      const int b = b0 + PAIR * (g + G * i);
-      const bool second = PAIR == 2 && b + 1 < b1;  // pair partner exists in this unit
-      const int slot = int((it + i) % S);
-      const uint32_t buf = ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes);
-      ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
-
-      uint32_t re[32], im[32];
-      // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) --
+  // One tile: column block (q, rb) of transform b (and b+1 for pairs) from
+  // ring buffer `buf`; release() hands the slot back to TMA after its last read.
+  auto tile = [&](long long q, int rb, int b, bool second, uint32_t buf, auto&& release) {
+    uint32_t re[32], im[32];
+    // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) --
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
-        if constexpr (PAIR == 2) {  // (re0,re1), (im0,im1) from the two halves
-          const uint32_t e = buf + (((warp + (c << S1)) << 5) + lane) * EB;
-          const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
-          re[c] = __byte_perm(lo, hi, 0x5410);
-          im[c] = __byte_perm(lo, hi, 0x7632);
-          if constexpr (CONJ_IN) im[c] = A::neg(im[c]);  // conj on load (fft.cpp:90-91)
-        } else if constexpr (A::kWords == 1) {
-          re[c] = ptx::lds32(a);
-          if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
-        } else {
-          ptx::lds64(a, re[c], im[c]);
-          if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
-        }
-      }
-#pragma unroll
-      for (int pl = 0; pl < 5; ++pl) {
-        uint32_t nre[32], nim[32];
-#pragma unroll
-        for (int rl = 0; rl < (1 << pl); ++rl) {
-          const int slot1 = (1 << pl) - 1 + rl;
-          const uint4 tw = FIRST ? ptx::lds128(tw_base + slot1 * 16)
-                                 : ptx::lds128(tw_base + (slot1 * 32 + lane) * 16);
-#pragma unroll
-          for (int qq = 0; qq < (16 >> pl); ++qq) {
-            const int jl = (qq << pl) | rl;
-            const int oa = (qq << (pl + 1)) + rl;
-            butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa],
-                                   nim[oa], nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-          }
-        }
-#pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          re[x] = nre[x];
-          if constexpr (A::kWords == 2) im[x] = nim[x];
-        }
-      }
-      // ---- exchange through the padded slot: [col][local pos] ---------------
-      group_sync();  // every stage-1 read of the TMA tile is done
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
-        if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
-      }
-      group_sync();
-      // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
-      // column output), later groups lanes walk columns (contiguous rows)
-#pragma unroll
-      for (int j = 0; j < NG2; ++j) {
-        const int col = FIRST ? warp + (j << S1) : lane;
-        const int rl_ = FIRST ? lane : warp + (j << S1);
-#pragma unroll
-        for (int c = 0; c < (1 << S1); ++c) {
-          const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
-          const int v = (j << S1) + c;
-          if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
-        }
-      }
-      // release the slot to this group's tile S ahead
-      ptx::fence_proxy_async_smem();
-      group_sync();
-      if (leader && i + S < k) issue_load(q, rb, b + PAIR * G * S, slot);
-      // ---- stage 2 ----------------------------------------------------------
-      const uint4* tw2 = FIRST ? nullptr
-                               : p.tw + (long long)rb * mp_block_records(S1) + 31 * 32 +
-                                     warp * 32 + lane;
-#pragma unroll
-      for (int pl = 0; pl < S1; ++pl) {
-        uint32_t nre[32], nim[32];
-#pragma unroll
-        for (int rl = 0; rl < (1 << pl); ++rl)
-#pragma unroll
-          for (int j = 0; j < NG2; ++j) {
-            const int slot2 = (1 << pl) - 1 + rl;
-            uint4 tw;
-            if constexpr (FIRST)
-              tw = ptx::lds128(tw_base + (31 + (slot2 << 5) + lane) * 16);
-            else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
-              tw = ptx::lds128(tw_base + (31 * 32 + (warp << 5) + lane +
-                                          (((slot2 << 5) + (j << S1)) << 5)) * 16);
-            else  // r_l = warp + 2^S1 j
-              tw = __ldg(tw2 + ((slot2 << 5) + (j << S1)) * 32);
-#pragma unroll
-            for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
-              const int jl = (qq << pl) | rl;
-              const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
-              const int oa = (j << S1) + (qq << (pl + 1)) + rl;
-              butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
-                                     nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-            }
-          }
-#pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          re[x] = nre[x];
-          if constexpr (A::kWords == 2) im[x] = nim[x];
-        }
-      }
-      // ---- scatter: q*2^(P+s) + r + 2^P*(r_l + 32 c') ------------------------
-      // element offsets in units of one stored complex (EB bytes)
-      uint8_t* gout = p.out + b * N * EB;
-      uint8_t* base;
-      long long cstride;  // bytes between output rows c'
-      if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
-        base = gout + ((q * 32 + warp) * L + lane) * EB;
-        cstride = 32 * EB;
+    for (int c = 0; c < 32; ++c) {
+      [[maybe_unused]] const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
+      if constexpr (PAIR == 2) {  // (re0,re1), (im0,im1) from the two halves
+        const uint32_t e = buf + (((warp + (c << S1)) << 5) + lane) * EB;
+        const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
+        re[c] = __byte_perm(lo, hi, 0x5410);
+        im[c] = __byte_perm(lo, hi, 0x7632);
+        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);  // conj on load (fft.cpp:90-91)
+      } else if constexpr (A::kWords == 1) {
+        re[c] = ptx::lds32(a);
+        if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
       } else {
-        base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * EB;
-        cstride = ((long long)EB << P) * 32;
+        ptx::lds64(a, re[c], im[c]);
+        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
+      }
+    }
+#pragma unroll
+    for (int pl = 0; pl < 5; ++pl) {
+      uint32_t nre[32], nim[32];
+#pragma unroll
+      for (int rl = 0; rl < (1 << pl); ++rl) {
+        const int slot1 = (1 << pl) - 1 + rl;
+        const uint4 tw = FIRST ? load_rec<A>(tw_base + slot1 * RB)
+                               : load_rec<A>(tw_base + (slot1 * 32 + lane) * RB);
+#pragma unroll
+        for (int qq = 0; qq < (16 >> pl); ++qq) {
+          const int jl = (qq << pl) | rl;
+          const int oa = (qq << (pl + 1)) + rl;
+          butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa],
+                                 nim[oa], nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
+        }
       }
 #pragma unroll
-      for (int j = 0; j < NG2; ++j)
+      for (int x = 0; x < 32; ++x) {
+        re[x] = nre[x];
+        if constexpr (A::kWords == 2) im[x] = nim[x];
+      }
+    }
+    // ---- exchange through the padded slot: [col][local pos] ---------------
+    group_sync();  // every stage-1 read of the TMA tile is done
 #pragma unroll
-        for (int c = 0; c < (1 << S1); ++c) {
-          const int v = (j << S1) + c;
-          uint32_t xr = re[v], xi = im[v];
-          if constexpr (SCALE_OUT) {  // conj + 1/n, one rounded mul each (fft.cpp:94-98)
-            if constexpr (A::kWords == 1) {
-              xr = A::mul(xr ^ 0x80000000u, p.scale);
-            } else {
-              xr = A::mul(xr, p.scale);
-              xi = A::mul(A::neg(xi), p.scale);
-            }
-          }
-          uint8_t* dst;
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
+      if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
+    }
+    group_sync();
+    // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
+    // column output), later groups lanes walk columns (contiguous rows)
+#pragma unroll
+    for (int j = 0; j < NG2; ++j) {
+      const int col = FIRST ? warp + (j << S1) : lane;
+      const int rl_ = FIRST ? lane : warp + (j << S1);
+#pragma unroll
+      for (int c = 0; c < (1 << S1); ++c) {
+        const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
+        const int v = (j << S1) + c;
+        if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
+      }
+    }
+    // release the slot to this group's tile S ahead
+    ptx::fence_proxy_async_smem();
+    group_sync();
+    release();
+    // ---- stage 2 ----------------------------------------------------------
+    [[maybe_unused]] const uint8_t* tw2 =
+        FIRST ? nullptr
+              : reinterpret_cast<const uint8_t*>(p.tw) +
+                    ((long long)rb * mp_block_records(S1) + 31 * 32 + warp * 32 + lane) * RB;
+#pragma unroll
+    for (int pl = 0; pl < S1; ++pl) {
+      uint32_t nre[32], nim[32];
+#pragma unroll
+      for (int rl = 0; rl < (1 << pl); ++rl)
+#pragma unroll
+        for (int j = 0; j < NG2; ++j) {
+          const int slot2 = (1 << pl) - 1 + rl;
+          uint4 tw;
           if constexpr (FIRST)
-            dst = base + ((long long)(j << S1) * L) * EB + c * cstride;
-          else
-            dst = base + (((long long)(j << S1) * EB) << P) + c * cstride;
-          if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
-            unsigned int* d0 = reinterpret_cast<unsigned int*>(dst);
-            unsigned int* d1 = reinterpret_cast<unsigned int*>(dst + N * EB);
-            const uint32_t t0 = __byte_perm(xr, xi, 0x5410), t1 = __byte_perm(xr, xi, 0x7632);
-            if constexpr (LAST) {
-              __stcs(d0, t0);
-              if (second) __stcs(d1, t1);
-            } else {
-              __stcg(d0, t0);
-              if (second) __stcg(d1, t1);
-            }
-          } else if constexpr (A::kWords == 1) {
-            if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
-            else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
-          } else {
-            if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
-            else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+            tw = load_rec<A>(tw_base + (31 + (slot2 << 5) + lane) * RB);
+          else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
+            tw = load_rec<A>(tw_base + (31 * 32 + (warp << 5) + lane +
+                                        (((slot2 << 5) + (j << S1)) << 5)) * RB);
+          else  // r_l = warp + 2^S1 j
+            tw = ldg_rec<A>(tw2 + ((slot2 << 5) + (j << S1)) * 32 * RB);
+#pragma unroll
+          for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
+            const int jl = (qq << pl) | rl;
+            const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
+            const int oa = (j << S1) + (qq << (pl + 1)) + rl;
+            butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
+                                   nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
           }
         }
+#pragma unroll
+      for (int x = 0; x < 32; ++x) {
+        re[x] = nre[x];
+        if constexpr (A::kWords == 2) im[x] = nim[x];
+      }
     }
-    it += k;
+    // ---- scatter ------------------------------------------------------------
+    // Stockham order: q*2^(P+s) + r + 2^P*(r_l + 32 c').  BOUT (the group
+    // feeding the last one) writes the blocked intermediate instead:
+    //   Z[(r' >> 5) * 2^s3 + c][r' & 31],  r' = r + 2^P c', c = q,
+    // so each last-group tile (32 columns r' x 2^s3 rows c) is one contiguous
+    // block.  Element offsets in units of one stored complex (EB bytes).
+    uint8_t* gout = p.out + b * N * EB;
+    [[maybe_unused]] const long long S3 = N >> (P + Lay::s);  // rows of the last group (BOUT)
+    uint8_t* base;
+    long long jstride, cstride;  // bytes between values j<<S1 and rows c'
+    if constexpr (FIRST && BOUT) {  // r' = lane + 32 c, c-index = column
+      base = gout + ((q * 32 + warp) * 32 + lane) * EB;
+      jstride = 32LL * EB;
+      cstride = S3 * 32 * EB;
+    } else if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
+      base = gout + ((q * 32 + warp) * L + lane) * EB;
+      jstride = (long long)L * EB;
+      cstride = 32 * EB;
+    } else if constexpr (BOUT) {  // r' = rb*32 + lane + 2^P (warp + 2^S1 j + 32 c)
+      base = gout + (((rb + ((long long)warp << (P - 5))) * S3 + q) * 32 + lane) * EB;
+      jstride = (S3 * 32 * EB) << (P - 5);
+      cstride = ((S3 * 32 * EB) << (P - 5)) * 32;
+    } else {
+      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * EB;
+      jstride = (long long)EB << P;
+      cstride = ((long long)EB << P) * 32;
+    }
+#pragma unroll
+    for (int j = 0; j < NG2; ++j)
+#pragma unroll
+      for (int c = 0; c < (1 << S1); ++c) {
+        const int v = (j << S1) + c;
+        uint32_t xr = re[v];
+        [[maybe_unused]] uint32_t xi = im[v];
+        if constexpr (SCALE_OUT) {  // conj + 1/n, one rounded mul each (fft.cpp:94-98)
+          if constexpr (A::kWords == 1) {
+            xr = A::mul(xr ^ 0x80000000u, p.scale);
+          } else {
+            xr = A::mul(xr, p.scale);
+            xi = A::mul(A::neg(xi), p.scale);
+          }
+        }
+        uint8_t* dst = base + (j << S1) * jstride + c * cstride;
+        if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
+          unsigned int* d0 = reinterpret_cast<unsigned int*>(dst);
+          unsigned int* d1 = reinterpret_cast<unsigned int*>(dst + N * EB);
+          const uint32_t t0 = __byte_perm(xr, xi, 0x5410), t1 = __byte_perm(xr, xi, 0x7632);
+          if constexpr (LAST) {
+            __stcs(d0, t0);
+            if (second) __stcs(d1, t1);
+          } else {
+            __stcg(d0, t0);
+            if (second) __stcg(d1, t1);
+          }
+        } else if constexpr (A::kWords == 1) {
+          if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
+          else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
+        } else {
+          if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+          else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+        }
+      }
+  };
+
+  if constexpr (FIRST) {
+    // Tiles in transform-major order (column block fastest): a CTA walks all
+    // column blocks of one transform (pair) before the next, so the rows it
+    // reads share DRAM pages; the twiddles are column-independent.
+    const long long nblk = (N >> Lay::s) >> 5;
+    const long long total = nblk * ((p.nb + PAIR - 1) / PAIR);
+    const long long per = (total + gridDim.x - 1) / gridDim.x;
+    const long long t_begin = blockIdx.x * per;
+    const long long t_end = t_begin + per < total ? t_begin + per : total;
+    const long long first_idx = t_begin + g;
+    const int k = first_idx < t_end ? int((t_end - first_idx + G - 1) / G) : 0;
+    auto load_tile = [&](int i) {
+      const long long idx = first_idx + (long long)G * i;
+      const long long pr = idx / nblk;
+      issue_load(idx - pr * nblk, 0, int(pr * PAIR), i % S);
+    };
+    if (leader)
+      for (int i = 0; i < S && i < k; ++i) load_tile(i);
+    for (int i = 0; i < k; ++i) {
+      const long long idx = first_idx + (long long)G * i;
+      const long long pr = idx / nblk;
+      const int b = int(pr * PAIR);
+      const int slot = i % S;
+      ptx::mbar_wait(&bars[slot], uint32_t((i / S) & 1));
+      tile(idx - pr * nblk, 0, b, PAIR == 2 && b + 1 < nb,
+           ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
+             if (leader && i + S < k) load_tile(i + S);
+           });
+    }
+  } else {
+    const long long per = (p.tiles + gridDim.x - 1) / gridDim.x;
+    const long long t_begin = blockIdx.x * per;
+    const long long t_end = t_begin + per < p.tiles ? t_begin + per : p.tiles;
+    long long it = 0;  // this group's running tile count (ring slot / phase)
+    for (long long u0 = t_begin; u0 < t_end;) {
+      const long long tt = u0 / nb;  // column block of this unit
+      const int b0 = int(u0 - tt * nb);
+      const long long u1 = (tt + 1) * nb < t_end ? (tt + 1) * nb : t_end;
+      const int b1 = b0 + int(u1 - u0);
+      u0 = u1;
+      const long long q = tt / rblocks;
+      const int rb = int(tt - q * rblocks);
+      {  // the unit's twiddle slab, shared by every group
+        __syncthreads();
+        // block records start 16-byte aligned: mp_block_records(S1) * RB % 16 == 0
+        const uint4* src = p.tw + (long long)rb * mp_block_records(S1) * RB / 16;
+        for (int i = threadIdx.x; i < Lay::kSlabRecords * RB / 16; i += blockDim.x)
+          tws[i] = src[i];
+        __syncthreads();
+      }
+      const int units = (b1 - b0 + PAIR - 1) / PAIR;  // tiles (transform pairs for fp16)
+      const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
+      if (leader)
+        for (int i = 0; i < S && i < k; ++i)
+          issue_load(q, rb, b0 + PAIR * (g + G * i), int((it + i) % S));
+      for (int i = 0; i < k; ++i) {
+        const int b = b0 + PAIR * (g + G * i);
+        const int slot = int((it + i) % S);
+        ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
+        tile(q, rb, b, PAIR == 2 && b + 1 < b1,
+             ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
+               if (leader && i + S < k) issue_load(q, rb, b + PAIR * G * S, slot);
+             });
+      }
+      it += k;
+    }
   }
 }
 
@@ -379,6 +436,22 @@ EncodeFn encode_fn() {
 }
 
 std::vector<int> split_passes(int m, int max_s) {
+  // DSFFT_MP_SPLIT="a,b[,c]" overrides (tuning; ignored unless every group is
+  // 6..9 passes and they sum to m)
+  if (const char* env = std::getenv("DSFFT_MP_SPLIT")) {
+    std::vector<int> v;
+    int sum = 0;
+    bool ok = true;
+    for (const char* c = env; *c;) {
+      const int s = std::atoi(c);
+      ok = ok && s >= 6 && s <= 9;
+      v.push_back(s);
+      sum += s;
+      while (*c && *c != ',') ++c;
+      if (*c == ',') ++c;
+    }
+    if (ok && sum == m && v.size() >= 2) return v;
+  }
   // 2 groups up to m = 2*max_s, 3 beyond; every group 6..max_s passes
   // (max_s = 9 for one-word fp16 values, 8 for fp32: a 2-deep ring of
   // 32 x 2^s x 8-byte tiles must fit in shared memory)
@@ -410,6 +483,13 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
     r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (P + s == m) {  // last group: blocked intermediate {r_l, c, rb, b}
+    cuuint64_t dims[4] = {32, cuuint64_t(1) << s, N >> (s + 5), cuuint64_t(batch)};
+    cuuint64_t strides[3] = {32 * cuuint64_t(vb), (cuuint64_t(32) << s) * vb, N * vb};
+    cuuint32_t box[4] = {32, rows_box, 1, 1};
+    r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {  // {r (2^P), q (N/2^(P+s)), c (2^s), b}
     cuuint64_t dims[4] = {cuuint64_t(1) << P, N >> (P + s), cuuint64_t(1) << s,
                           cuuint64_t(batch)};
@@ -424,7 +504,7 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
 
 template <int S1, class A, bool STD>
 cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, bool conj_in,
-                        bool scale_out, bool last, int sm_count, size_t smem_optin,
+                        bool scale_out, bool last, bool bout, int sm_count, size_t smem_optin,
                         cudaStream_t st) {
   using Lay = MpLayout<S1, A>;
   MpParams q = p;
@@ -454,24 +534,28 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
     kern<<<grid, threads, smem, st>>>(map, q);
     return cudaGetLastError();
   };
-  if (first)  // never last: every split has >= 2 groups
-    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false>)
-                   : go(mp_kernel<S1, A, STD, true, false, false, false>);
+  // the group before the last writes the blocked intermediate (bout)
+  if (first && bout)  // never last: every split has >= 2 groups
+    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, true>)
+                   : go(mp_kernel<S1, A, STD, true, false, false, false, true>);
+  if (first)
+    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, false>)
+                   : go(mp_kernel<S1, A, STD, true, false, false, false, false>);
   if (last)
-    return scale_out ? go(mp_kernel<S1, A, STD, false, false, true, true>)
-                     : go(mp_kernel<S1, A, STD, false, false, false, true>);
-  return go(mp_kernel<S1, A, STD, false, false, false, false>);
+    return scale_out ? go(mp_kernel<S1, A, STD, false, false, true, true, false>)
+                     : go(mp_kernel<S1, A, STD, false, false, false, true, false>);
+  return go(mp_kernel<S1, A, STD, false, false, false, false, true>);  // middle of 3
 }
 
 template <class A, bool STD>
 cudaError_t mp_launch_a(int S1, const CUtensorMap& map, const MpParams& p, bool first,
-                        bool conj_in, bool scale_out, bool last, int sm_count, size_t optin,
-                        cudaStream_t st) {
+                        bool conj_in, bool scale_out, bool last, bool bout, int sm_count,
+                        size_t optin, cudaStream_t st) {
   switch (S1) {
-    case 1: return mp_launch_t<1, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
-    case 2: return mp_launch_t<2, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
-    case 3: return mp_launch_t<3, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
-    case 4: return mp_launch_t<4, A, STD>(map, p, first, conj_in, scale_out, last, sm_count, optin, st);
+    case 1: return mp_launch_t<1, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
+    case 2: return mp_launch_t<2, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
+    case 3: return mp_launch_t<3, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
+    case 4: return mp_launch_t<4, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -534,9 +618,9 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
               }
         }
     }
-    if (cudaMalloc(&g.d_tw, recs.size() * sizeof(Record)) != cudaSuccess ||
-        cudaMemcpy(g.d_tw, recs.data(), recs.size() * sizeof(Record), cudaMemcpyHostToDevice) !=
-            cudaSuccess) {
+    const std::vector<uint8_t> img = serialize_records(recs, record_bytes(precision, f16c));
+    if (cudaMalloc(&g.d_tw, img.size()) != cudaSuccess ||
+        cudaMemcpy(g.d_tw, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
       g_mp_err = "multipass: twiddle upload failed";
       mp->groups.push_back(g);
       delete mp;
@@ -612,19 +696,19 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       p.scale = scale;
       const bool first = i == 0, last = i == ng - 1;
       const int S1 = g.s - 5;
-      const bool ci = first && inverse, so = last && inverse;
+      const bool ci = first && inverse, so = last && inverse, bo = i == ng - 2;
       const int sm = mp.sm_count;
       const size_t oi = mp.smem_optin;
       cudaError_t e;
       if (f16 && mp.f16_pairs)
-        e = std_ ? mp_launch_a<ArithF16P, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
-                 : mp_launch_a<ArithF16P, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF16P, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF16P, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       else if (f16)
-        e = std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
-                 : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       else
-        e = std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, ci, so, last, sm, oi, stream)
-                 : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, ci, so, last, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       if (e != cudaSuccess) {
         g_mp_err = std::string("mp_kernel launch: ") + cudaGetErrorString(e);
         return 1;

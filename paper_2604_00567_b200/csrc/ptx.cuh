@@ -117,6 +117,18 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
                : "r"(a));
   return v;
 }
+// f16x2 half broadcasts (h, h).  Written as a b16 unpack/repack so ptxas
+// folds them into the consuming HFMA2/HMUL2 operand select (.H0_H0/.H1_H1).
+__device__ __forceinline__ uint32_t bcast_lo(uint32_t x) {
+  uint32_t d;
+  asm("{.reg .b16 l, h; mov.b32 {l, h}, %1; mov.b32 %0, {l, l};}" : "=r"(d) : "r"(x));
+  return d;
+}
+__device__ __forceinline__ uint32_t bcast_hi(uint32_t x) {
+  uint32_t d;
+  asm("{.reg .b16 l, h; mov.b32 {l, h}, %1; mov.b32 %0, {h, h};}" : "=r"(d) : "r"(x));
+  return d;
+}
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
