@@ -140,15 +140,19 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   constexpr int PAIR = A::kPair;
   constexpr int EB = A::kSampleBytes;           // bytes of one complex in memory
   constexpr int HALF = 32 * L * EB;             // one transform's tile
+  // fp16 pairs keep intermediates pair-packed: 8-byte values (re0,re1),(im0,im1)
+  // of transforms (b, b+1) at pair index b/2 -- no unpack/repack between groups
+  constexpr bool PIN = PAIR == 2 && !FIRST, POUT = PAIR == 2 && !LAST;
+  constexpr int OEB = POUT ? 8 : EB;            // bytes per stored output element
   auto issue_load = [&](long long q, int rb, int b, int slot) {
     uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
     ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
 #pragma unroll
-    for (int h = 0; h < PAIR; ++h)
+    for (int h = 0; h < (PIN ? 1 : PAIR); ++h)
 #pragma unroll
       for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
-        uint8_t* d = dst + h * HALF + size_t(r0) * 32 * EB;
-        const int bb = int(b + h + p.b_off);
+        uint8_t* d = dst + h * HALF + size_t(r0) * 32 * (PIN ? 8 : EB);
+        const int bb = PIN ? b / 2 : int(b + h + p.b_off);
         if constexpr (FIRST)
           ptx::tma_load_3d(d, &in_map, int(q * 32), r0, bb, &bars[slot], pol);
         else if constexpr (LAST)  // blocked intermediate {r_l, c, rb, b}
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       [[maybe_unused]] const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
-      if constexpr (PAIR == 2) {  // (re0,re1), (im0,im1) from the two halves
+      if constexpr (PAIR == 2 && !PIN) {  // (re0,re1), (im0,im1) from the two halves
         const uint32_t e = buf + (((warp + (c << S1)) << 5) + lane) * EB;
         const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
         re[c] = __byte_perm(lo, hi, 0x5410);
@@ -269,26 +273,26 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     //   Z[(r' >> 5) * 2^s3 + c][r' & 31],  r' = r + 2^P c', c = q,
     // so each last-group tile (32 columns r' x 2^s3 rows c) is one contiguous
     // block.  Element offsets in units of one stored complex (EB bytes).
-    uint8_t* gout = p.out + b * N * EB;
+    uint8_t* gout = p.out + b * N * EB;  // == pair b/2 * N * 8 for packed pairs
     [[maybe_unused]] const long long S3 = N >> (P + Lay::s);  // rows of the last group (BOUT)
     uint8_t* base;
     long long jstride, cstride;  // bytes between values j<<S1 and rows c'
     if constexpr (FIRST && BOUT) {  // r' = lane + 32 c, c-index = column
-      base = gout + ((q * 32 + warp) * 32 + lane) * EB;
-      jstride = 32LL * EB;
-      cstride = S3 * 32 * EB;
+      base = gout + ((q * 32 + warp) * 32 + lane) * OEB;
+      jstride = 32LL * OEB;
+      cstride = S3 * 32 * OEB;
     } else if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
-      base = gout + ((q * 32 + warp) * L + lane) * EB;
-      jstride = (long long)L * EB;
-      cstride = 32 * EB;
+      base = gout + ((q * 32 + warp) * L + lane) * OEB;
+      jstride = (long long)L * OEB;
+      cstride = 32 * OEB;
     } else if constexpr (BOUT) {  // r' = rb*32 + lane + 2^P (warp + 2^S1 j + 32 c)
-      base = gout + (((rb + ((long long)warp << (P - 5))) * S3 + q) * 32 + lane) * EB;
-      jstride = (S3 * 32 * EB) << (P - 5);
-      cstride = ((S3 * 32 * EB) << (P - 5)) * 32;
+      base = gout + (((rb + ((long long)warp << (P - 5))) * S3 + q) * 32 + lane) * OEB;
+      jstride = (S3 * 32 * OEB) << (P - 5);
+      cstride = ((S3 * 32 * OEB) << (P - 5)) * 32;
     } else {
-      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * EB;
-      jstride = (long long)EB << P;
-      cstride = ((long long)EB << P) * 32;
+      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * OEB;
+      jstride = (long long)OEB << P;
+      cstride = ((long long)OEB << P) * 32;
     }
 #pragma unroll
     for (int j = 0; j < NG2; ++j)
@@ -306,7 +310,9 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
           }
         }
         uint8_t* dst = base + (j << S1) * jstride + c * cstride;
-        if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
+        if constexpr (POUT) {  // pair-packed intermediate
+          __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
+        } else if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
           unsigned int* d0 = reinterpret_cast<unsigned int*>(dst);
           unsigned int* d1 = reinterpret_cast<unsigned int*>(dst + N * EB);
           const uint32_t t0 = __byte_perm(xr, xi, 0x5410), t1 = __byte_perm(xr, xi, 0x7632);
@@ -357,15 +363,18 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
            });
     }
   } else {
-    const long long per = (p.tiles + gridDim.x - 1) / gridDim.x;
+    // units of PAIR transforms, column block outer: tile u -> (tt, pair v)
+    const long long nbu = (p.nb + PAIR - 1) / PAIR;
+    const long long total = ((N >> Lay::s) >> 5) * nbu;
+    const long long per = (total + gridDim.x - 1) / gridDim.x;
     const long long t_begin = blockIdx.x * per;
-    const long long t_end = t_begin + per < p.tiles ? t_begin + per : p.tiles;
+    const long long t_end = t_begin + per < total ? t_begin + per : total;
     long long it = 0;  // this group's running tile count (ring slot / phase)
     for (long long u0 = t_begin; u0 < t_end;) {
-      const long long tt = u0 / nb;  // column block of this unit
-      const int b0 = int(u0 - tt * nb);
-      const long long u1 = (tt + 1) * nb < t_end ? (tt + 1) * nb : t_end;
-      const int b1 = b0 + int(u1 - u0);
+      const long long tt = u0 / nbu;  // column block of this unit
+      const int v0 = int(u0 - tt * nbu);
+      const long long u1 = (tt + 1) * nbu < t_end ? (tt + 1) * nbu : t_end;
+      const int units = int(u1 - u0);
       u0 = u1;
       const long long q = tt / rblocks;
       const int rb = int(tt - q * rblocks);
@@ -377,16 +386,15 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
           tws[i] = src[i];
         __syncthreads();
       }
-      const int units = (b1 - b0 + PAIR - 1) / PAIR;  // tiles (transform pairs for fp16)
       const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
       if (leader)
         for (int i = 0; i < S && i < k; ++i)
-          issue_load(q, rb, b0 + PAIR * (g + G * i), int((it + i) % S));
+          issue_load(q, rb, PAIR * (v0 + g + G * i), int((it + i) % S));
       for (int i = 0; i < k; ++i) {
-        const int b = b0 + PAIR * (g + G * i);
+        const int b = PAIR * (v0 + g + G * i);
         const int slot = int((it + i) % S);
         ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
-        tile(q, rb, b, PAIR == 2 && b + 1 < b1,
+        tile(q, rb, b, PAIR == 2 && b + 1 < nb,
              ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
                if (leader && i + S < k) issue_load(q, rb, b + PAIR * G * S, slot);
              });
@@ -652,7 +660,9 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const size_t chunk = std::min(mp.chunk_transforms, batch);
   uint8_t* scratch[2] = {nullptr, nullptr};
   for (int i = 0; i < std::min(ng - 1, 2); ++i)
-    if (scratch_alloc(reinterpret_cast<void**>(&scratch[i]), chunk * tb, stream) !=
+    // pair-packed fp16 intermediates hold whole pairs: round up to even
+    if (scratch_alloc(reinterpret_cast<void**>(&scratch[i]), ((chunk + 1) & ~size_t(1)) * tb,
+                      stream) !=
         cudaSuccess) {
       for (auto* sp : scratch) scratch_free(sp, stream);
       g_mp_err = "multipass: scratch allocation failed";
@@ -672,7 +682,11 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   for (int i = 0; i < ng; ++i) {
     const void* base = i == 0 ? in : scratch[(i - 1) & 1];
     const long long nb = i == 0 ? (long long)batch : (long long)chunk;
-    const int rc = make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s, vb, nb);
+    // groups after the first read pair-packed fp16 intermediates: 8-byte
+    // elements, one map "batch" entry per transform pair
+    const bool packed = i > 0 && f16 && mp.f16_pairs;
+    const int rc = make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s,
+                               packed ? 8 : vb, packed ? (nb + 1) / 2 : nb);
     if (rc != 0) {
       g_mp_err = "multipass: cuTensorMapEncodeTiled failed (CUresult " + std::to_string(rc) +
                  ", group " + std::to_string(i) + ", base " +

@@ -213,6 +213,25 @@ def test_multipass_many_chunks(dsfft, cuda, orc):
     assert bit_mismatches(y[idx], want) == 0
 
 
+@pytest.mark.parametrize("n,precision,chunk_mb,batch", [
+    (1 << 18, "fp16", 3, 7),   # 3 transforms per chunk: odd chunks, pair straddles
+    (1 << 16, "fp16", 1, 9),   # 4 per chunk, odd tail
+    (1 << 20, "fp16", 5, 3),   # 3 pass groups, 1 transform per chunk
+    (1 << 16, "fp32", 3, 5)])
+@pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
+def test_multipass_odd_chunks(dsfft, cuda, orc, monkeypatch, n, precision, chunk_mb, batch,
+                              inverse):
+    """Chunked batches whose chunks hold an odd number of transforms: fp16
+    pair-packed intermediates and pair partners across chunk boundaries."""
+    monkeypatch.setenv("DSFFT_MP_CHUNK_MB", str(chunk_mb))
+    chk = _checker()
+    x = ref_inputs(orc, n, batch, seed=n + batch, precision=precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+    want = to_work((chk.inverse if inverse else chk.forward)(x, "dual", precision), precision)
+    assert bit_mismatches(y, want) == 0
+
+
 @pytest.mark.parametrize("n,precision", [(1024, "fp16"), (1 << 16, "fp16"), (1 << 14, "fp32"),
                                          (256, "fp64"), (2, "fp16")])
 def test_one_plan_many_streams(dsfft, cuda, orc, n, precision):
