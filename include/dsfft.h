@@ -96,6 +96,21 @@ int dsfft_build_table(size_t n, int strategy, int precision, double clamp_eps, d
 size_t dsfft_table_csv(size_t n, int strategy, int precision, double clamp_eps, char* out,
                        size_t cap);
 
+/* Ratio statistics and error bounds in the reference's CSV schema,
+ * write_bounds_csv (serialize.cpp:79-91: "strategy,t_max,argmax_k,
+ * singular_count,cos_path_count,sin_path_count,per_butterfly_bound,
+ * cumulative_bound,improvement_vs_baseline,divergent"):
+ *   kind DSFFT_STATS_RATIO      reproduce_ratio_table(n) (analysis.cpp:65-76),
+ *                               the CLI `stats` command (main.cpp:45-52):
+ *                               LF, cosine, dual at binary16 epsilon;
+ *   kind DSFFT_STATS_CUMULATIVE reproduce_cumulative_table(n, precision)
+ *                               (analysis.cpp:78-88), the CLI `bounds`: LF, dual.
+ * Statistics come from the FP64 tables (table_stats, twiddle.cpp:143-162).
+ * Returns the bytes needed including the NUL (0 on error); copies when `cap`
+ * suffices. */
+enum { DSFFT_STATS_RATIO = 0, DSFFT_STATS_CUMULATIVE = 1 };
+size_t dsfft_bounds_csv(size_t n, int kind, int precision, char* out, size_t cap);
+
 /* Copy of the plan's rounded table: FftPlan::table.entries (n/2 records). */
 int dsfft_plan_table(dsfft_plan plan, dsfft_entry* out, size_t count);
 

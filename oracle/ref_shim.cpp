@@ -254,5 +254,23 @@ size_t ref_table_csv(std::size_t n, int s, int p, double clamp_eps, char* out, s
   if (out && cap > str.size()) std::memcpy(out, str.c_str(), str.size() + 1);
   return str.size() + 1;
 }
+
+// write_bounds_csv (serialize.cpp:79-91) of reproduce_ratio_table(n) (kind 0,
+// the CLI `stats` command) or reproduce_cumulative_table(n, p) (kind 1, `bounds`).
+size_t ref_bounds_csv(std::size_t n, int kind, int p, char* out, size_t cap) {
+  std::ostringstream os;
+  try {
+    if (kind == 0)
+      fmafft::write_bounds_csv(os, fmafft::reproduce_ratio_table(n));
+    else
+      fmafft::write_bounds_csv(os, fmafft::reproduce_cumulative_table(n, P(p)));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 0;
+  }
+  const std::string str = os.str();
+  if (out && cap > str.size()) std::memcpy(out, str.c_str(), str.size() + 1);
+  return str.size() + 1;
+}
 }
 #endif

@@ -160,6 +160,25 @@ def make_plan(n: int, strategy: str = "dual", precision: str = "fp32",
     return FftPlan(int(n), m, strategy, precision, device, h)
 
 
+def bounds_csv(n: int, kind: str = "stats", precision: str = "fp16") -> str:
+    """write_bounds_csv (serialize.cpp:79-91) of reproduce_ratio_table(n)
+    (kind "stats": the CLI `stats` command) or reproduce_cumulative_table(n,
+    precision) (kind "bounds")."""
+    kinds = {"stats": 0, "ratio": 0, "bounds": 1, "cumulative": 1}
+    if kind not in kinds:
+        raise ValueError(f"unknown statistics kind: {kind}")
+    lib = _load()
+    lib.dsfft_bounds_csv.restype = C.c_size_t
+    lib.dsfft_bounds_csv.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+    args = (int(n), kinds[kind], PRECISIONS[parse_precision(precision)])
+    need = lib.dsfft_bounds_csv(*args, None, 0)
+    if need == 0:
+        raise ValueError(lib.dsfft_last_error().decode())
+    buf = C.create_string_buffer(need)
+    lib.dsfft_bounds_csv(*args, buf, need)
+    return buf.value.decode()
+
+
 def table_csv(n: int, strategy: str, precision: str = "fp64", clamp_eps: float = 1e-7) -> str:
     """write_table_csv (serialize.cpp:48-57) of build_table (fp64, the CLI
     `twiddles` dump) or of the plan's rounded table (fp16 / fp32)."""

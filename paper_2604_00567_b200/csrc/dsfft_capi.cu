@@ -421,6 +421,82 @@ size_t dsfft_table_csv(size_t n, int strategy, int precision, double clamp_eps, 
   return s.size() + 1;
 }
 
+size_t dsfft_bounds_csv(size_t n, int kind, int precision, char* out, size_t cap) {
+  if (kind != DSFFT_STATS_RATIO && kind != DSFFT_STATS_CUMULATIVE) {
+    fail(DSFFT_ERR_INVALID, "unknown statistics kind");
+    return 0;
+  }
+  if (kind == DSFFT_STATS_CUMULATIVE && (precision < 0 || precision > 2)) {
+    fail(DSFFT_ERR_INVALID, "unknown precision");
+    return 0;
+  }
+  // machine_epsilon (precision.cpp:36-43); the ratio table is quoted at fp16
+  const double eps = kind == DSFFT_STATS_RATIO || precision == dsfft::kFp16 ? 0x1p-11
+                     : precision == dsfft::kFp32                           ? 0x1p-24
+                                                                           : 0x1p-53;
+  struct Row {
+    int strategy;
+    double t_max = 0.0, per = 0.0, cum = 0.0, improvement = 1.0;
+    size_t argmax = 0, singular = 0, ncos = 0, nsin = 0;
+  };
+  std::vector<Row> rows;
+  const std::vector<int> strategies =
+      kind == DSFFT_STATS_RATIO
+          ? std::vector<int>{dsfft::kLinzerFeig, dsfft::kCosine, dsfft::kDual}
+          : std::vector<int>{dsfft::kLinzerFeig, dsfft::kDual};
+  try {
+    for (int st : strategies) {
+      const std::vector<dsfft::TableEntry> t = dsfft::build_table(n, st, 1e-7);
+      Row r;
+      r.strategy = st;
+      for (size_t k = 0; k < t.size(); ++k) {  // table_stats (twiddle.cpp:143-162)
+        (t[k].path == dsfft::kCos ? r.ncos : r.nsin)++;
+        if (t[k].clamped) {
+          ++r.singular;
+          continue;
+        }
+        const double a = std::fabs(t[k].ratio);
+        if (a > r.t_max) {
+          r.t_max = a;
+          r.argmax = k;
+        }
+      }
+      // per_butterfly_bound / cumulative_bound (analysis.cpp:59-63), m = log2 n
+      r.per = r.t_max * eps;
+      r.cum = std::pow(1.0 + r.t_max * eps, double(__builtin_ctzll(n))) - 1.0;
+      rows.push_back(r);
+    }
+  } catch (const std::exception& e) {
+    fail(DSFFT_ERR_INVALID, e.what());
+    return 0;
+  }
+  for (size_t i = 1; i < rows.size(); ++i) rows[i].improvement = rows[0].cum / rows[i].cum;
+  std::string s =
+      "strategy,t_max,argmax_k,singular_count,cos_path_count,sin_path_count,"
+      "per_butterfly_bound,cumulative_bound,improvement_vs_baseline,divergent\n";
+  char buf[48];
+  auto num = [&](double v) {  // format_double: %.17g (serialize.cpp:42-46)
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    s += buf;
+  };
+  static const char* kNames[] = {"standard", "lf", "cosine", "dual"};  // twiddle.cpp:31-39
+  for (const Row& r : rows) {
+    s += kNames[r.strategy];
+    s += ',';
+    num(r.t_max);
+    s += ',' + std::to_string(r.argmax) + ',' + std::to_string(r.singular) + ',' +
+         std::to_string(r.ncos) + ',' + std::to_string(r.nsin) + ',';
+    num(r.per);
+    s += ',';
+    num(r.cum);
+    s += ',';
+    num(r.improvement);
+    s += r.per >= 1.0 ? ",true\n" : ",false\n";
+  }
+  if (out && cap > s.size()) std::memcpy(out, s.c_str(), s.size() + 1);
+  return s.size() + 1;
+}
+
 int dsfft_plan_table(dsfft_plan p, dsfft_entry* out, size_t count) {
   if (!p || !out) return fail(DSFFT_ERR_INVALID, "null argument");
   if (count < p->table.size()) return fail(DSFFT_ERR_INVALID, "output too small");

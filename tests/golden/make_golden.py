@@ -82,6 +82,18 @@ def main():
             lib.ref_table_csv(n, s, p, 1e-7, buf, need)
             out[f"csv/{n}/{STRATS[s]}/{('fp16', 'fp32', 'fp64')[p]}"] = \
                 np.frombuffer(buf.value, dtype=np.uint8)
+    # write_bounds_csv of reproduce_ratio_table / reproduce_cumulative_table
+    # (the CLI `stats` and `bounds` commands)
+    if hasattr(lib, "ref_bounds_csv"):
+        lib.ref_bounds_csv.restype = C.c_size_t
+        lib.ref_bounds_csv.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+        for n, kind, p in ((1024, 0, 0), (64, 0, 0), (1 << 20, 0, 0), (2, 0, 0),
+                           (1024, 1, 0), (1024, 1, 1), (4096, 1, 2), (8, 1, 0)):
+            need = lib.ref_bounds_csv(n, kind, p, None, 0)
+            buf = C.create_string_buffer(need)
+            lib.ref_bounds_csv(n, kind, p, buf, need)
+            out[f"bounds/{n}/{('stats', 'bounds')[kind]}/{('fp16', 'fp32', 'fp64')[p]}"] = \
+                np.frombuffer(buf.value, dtype=np.uint8)
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes,", len(out), "arrays")

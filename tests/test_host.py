@@ -70,6 +70,29 @@ def test_table_csv_matches_reference_writer(dsfft):
         dsfft.table_csv(12, "dual")
 
 
+def test_bounds_csv_matches_reference_writer(dsfft):
+    """dsfft_bounds_csv == write_bounds_csv (serialize.cpp:79-91) of
+    reproduce_ratio_table / reproduce_cumulative_table (analysis.cpp:65-88),
+    byte for byte (golden dumps from the reference's own code)."""
+    g = np.load(GOLDEN)
+    keys = [k for k in g.files if k.startswith("bounds/")]
+    assert len(keys) >= 8
+    for key in keys:
+        _, n, kind, p = key.split("/")
+        assert dsfft.bounds_csv(int(n), kind, p).encode() == g[key].tobytes(), key
+    text = dsfft.bounds_csv(1024, "stats")
+    rows = [r.split(",") for r in text.strip().split("\n")[1:]]
+    # Table I (PAPER.md:146-150): LF t_max 163 at k=1, dual 1.0, one LF singularity
+    assert [r[0] for r in rows] == ["lf", "cosine", "dual"]
+    assert abs(float(rows[0][1]) - 162.97) < 0.01 and rows[0][2] == "1" and rows[0][3] == "1"
+    assert abs(float(rows[2][1]) - 1.0) < 1e-15 and rows[2][3] == "0"
+    assert abs(float(rows[2][8]) - 235.1) < 0.01  # dual vs LF (PAPER.md:164)
+    with pytest.raises(ValueError, match="power of two"):
+        dsfft.bounds_csv(1000)
+    with pytest.raises(ValueError, match="unknown statistics kind"):
+        dsfft.bounds_csv(64, "histogram")
+
+
 def test_ingest_rounding_matches_oracle(dsfft, orc):
     rng = np.random.RandomState(916)
     x = (1 + rng.randint(0, 1 << 52, 300000) * 2.0 ** -52) * np.exp2(rng.randint(-30, 21, 300000))

@@ -1,0 +1,27 @@
+#!/bin/bash
+# Config-3 / config-5 sweep (BASELINE.json): every N x precision x variant
+# through bench.py, one JSON line each -> gpurun_out/sweep.jsonl.
+#   tools/gpu_sweep.sh            (run under gpurun; format with tools/sweep_table.py)
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+out=gpurun_out/sweep.jsonl
+: > "$out"
+NS=${NS:-"64 128 256 512 1024 2048 4096"}
+LARGE=${LARGE:-"8192 65536 262144 1048576 16777216"}
+for n in $NS; do
+  for p in fp16 fp32; do
+    for s in ${STRATS:-standard lf cosine dual}; do
+      timeout 300 python bench.py --n "$n" --precision "$p" --strategy "$s" --steps "${STEPS:-30}" \
+        --warmup 3 --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
+    done
+  done
+done
+for n in $LARGE; do
+  for p in fp16 fp32; do
+    for s in ${LSTRATS:-standard dual}; do
+      timeout 300 python bench.py --n "$n" --precision "$p" --strategy "$s" --steps "${STEPS:-30}" \
+        --warmup 3 --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
+    done
+  done
+done
+wc -l "$out"
