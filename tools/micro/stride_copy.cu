@@ -43,6 +43,35 @@ __global__ void plain_copy(const uint4* __restrict__ in, uint4* __restrict__ out
     __stcs(out + i, __ldcs(in + i));
 }
 
+template <typename T>
+__global__ void copy_w(const T* __restrict__ in, T* __restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    __stcs(out + i, __ldcs(in + i));
+}
+// 16-byte loads, W-byte stores (the loaded vector written as 16/W stores)
+template <int W>
+__global__ void copy_st(const uint4* __restrict__ in, char* __restrict__ out, long long n) {
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nthr) {
+    const uint4 v = __ldcs(in + i);
+    // lane-interleaved so each store instruction covers contiguous lines:
+    // element j of thread t goes to (block base) + j * (32 * W) + lane * W
+    const long long warp_base = (i - (threadIdx.x & 31)) * 16;
+    const int lane = threadIdx.x & 31;
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (W == 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) __stcs(reinterpret_cast<unsigned*>(out + warp_base + j * 128 + lane * 4), w[j]);
+    } else if constexpr (W == 8) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) __stcs(reinterpret_cast<uint2*>(out + warp_base + j * 256 + lane * 8), make_uint2(w[2*j], w[2*j+1]));
+    } else {
+      __stcs(reinterpret_cast<uint4*>(out + warp_base + lane * 16), v);
+    }
+  }
+}
+
 int main() {
   const long long bytes = 1LL << 30;
   uint4 *a, *b;
@@ -59,6 +88,13 @@ int main() {
     return 2.0 * bytes / (ms / 10 * 1e-3) / 1e9;
   };
   printf("plain copy: %.0f GB/s\n", timeit([&] { plain_copy<<<sms * 8, 256>>>(a, b, bytes / 16); }));
+  printf("copy 4-byte ld/st: %.0f GB/s\n", timeit([&] { copy_w<unsigned><<<sms * 8, 256>>>((const unsigned*)a, (unsigned*)b, bytes / 4); }));
+  printf("copy 8-byte ld/st: %.0f GB/s\n", timeit([&] { copy_w<uint2><<<sms * 8, 256>>>((const uint2*)a, (uint2*)b, bytes / 8); }));
+  for (int occ : {2, 4, 8}) {
+    printf("16-B loads, 4-B stores, %d CTAs/SM: %.0f GB/s\n", occ, timeit([&] { copy_st<4><<<sms * occ, 256>>>(a, (char*)b, bytes / 16); }));
+    printf("16-B loads, 8-B stores, %d CTAs/SM: %.0f GB/s\n", occ, timeit([&] { copy_st<8><<<sms * occ, 256>>>(a, (char*)b, bytes / 16); }));
+    printf("16-B loads, 16-B stores, %d CTAs/SM: %.0f GB/s\n", occ, timeit([&] { copy_st<16><<<sms * occ, 256>>>(a, (char*)b, bytes / 16); }));
+  }
   // N = 2^16 fp16 complex (4 B): transform 256 KB, 256 rows x 1 KB
   struct Case { long long tb; int rows; long long rs; };
   for (Case c : {Case{1 << 18, 256, 1024}, Case{1 << 15, 128, 256}, Case{1 << 22, 256, 16384}}) {
