@@ -51,10 +51,11 @@ SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
   e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
   // Defaults from B200 sweeps (profiles/README.md, "launch shapes"):
-  // fp16 one-complex-per-register wins for N <= 512 (94% of HBM at 512),
-  // transform pairs for N >= 1024 (98% at 1024); N >= 2048 is shared-memory
-  // bound (twiddles ~N*16 B), where a 1-deep ring with more groups wins.
-  e.f16_default = (DSFFT_M == 10 || DSFFT_M == 12) ? kVarF16P : kVarF16C;
+  // with 8-byte records, fp16 transform pairs win from N = 256 (97% of HBM vs
+  // 87% one-complex) up; one complex per register for N <= 128.  N >= 2048 is
+  // shared-memory bound (per-stage twiddle tables ~N*8 B plus 32 KB items),
+  // where a 1-deep ring with more groups wins.
+  e.f16_default = DSFFT_M >= 8 ? kVarF16P : kVarF16C;
   e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : 3;
   e.stages[kVarF16P] = DSFFT_M >= 11 ? 1 : 2;
   e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : 2;
