@@ -177,7 +177,7 @@ LARGE = [2 ** m for m in range(13, 21)]
 @pytest.mark.parametrize("n", LARGE)
 @pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
 def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
-    """N = 2^13..2^20: 2-3 pass-group launches, L2-chunked batch."""
+    """N = 2^13..2^20: 2-3 pass-group launches."""
     chk = _checker()
     batch = 3 if n <= 1 << 16 else 2
     strategies = ALL_STRATEGIES if n <= 1 << 14 else ("dual", "lf")
@@ -187,6 +187,22 @@ def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
         y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
         want = to_work((chk.inverse if inverse else chk.forward)(x, s, precision), precision)
         assert bit_mismatches(y, want) == 0, (n, s, precision)
+
+
+@pytest.mark.parametrize("n", [1 << 15, 1 << 17, 1 << 19])
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+@pytest.mark.parametrize("strategy", ["standard", "cosine"])
+def test_multipass_other_variants(dsfft, cuda, orc, n, precision, strategy):
+    """Standard and cosine through 2- and 3-group splits (cosine fp16 overflows
+    to non-finite exactly where the reference does; compared as both-NaN)."""
+    chk = _checker()
+    x = ref_inputs(orc, n, 2, seed=n + 11, precision=precision)
+    for inverse in (False, True):
+        plan = dsfft.make_plan(n, strategy, precision)
+        y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+        want = to_work((chk.inverse if inverse else chk.forward)(x, strategy, precision),
+                       precision)
+        assert bit_mismatches(y, want) == 0, (n, strategy, precision, inverse)
 
 
 @pytest.mark.parametrize("m", [21, 22, 23, 24])
