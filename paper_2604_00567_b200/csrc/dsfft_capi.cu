@@ -260,11 +260,14 @@ int launch(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch,
   return DSFFT_OK;
 }
 
-int check_exec_args(dsfft_plan_s* p, int dir, const void* in, void* out) {
+int check_exec_args(dsfft_plan_s* p, int dir, const void* in, void* out, size_t batch) {
   if (!p) return fail(DSFFT_ERR_INVALID, "null plan");
   if (dir != DSFFT_FORWARD && dir != DSFFT_INVERSE)
     return fail(DSFFT_ERR_INVALID, "unknown direction");
   if (!in || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
+  // byte counts (and the f64 carrier's 16 B per sample) must fit in size_t
+  if (batch > (SIZE_MAX / 16) / p->n)
+    return fail(DSFFT_ERR_INVALID, "batch too large: byte count overflows size_t");
   return DSFFT_OK;
 }
 
@@ -509,7 +512,7 @@ int dsfft_plan_table(dsfft_plan p, dsfft_entry* out, size_t count) {
 
 int dsfft_execute(dsfft_plan p, int dir, const void* in, void* out, size_t batch, void* stream) {
   g_launches = 0;
-  int rc = check_exec_args(p, dir, in, out);
+  int rc = check_exec_args(p, dir, in, out, batch);
   if (rc) return rc;
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(DSFFT_ERR_INVALID, "device buffers must be 16-byte aligned");
@@ -520,7 +523,7 @@ int dsfft_execute(dsfft_plan p, int dir, const void* in, void* out, size_t batch
 int dsfft_execute_host(dsfft_plan p, int dir, const void* h_in, void* h_out, size_t batch,
                        void* stream_) {
   g_launches = 0;
-  int rc = check_exec_args(p, dir, h_in, h_out);
+  int rc = check_exec_args(p, dir, h_in, h_out, batch);
   if (rc) return rc;
   if (batch == 0) return DSFFT_OK;
   DeviceGuard guard(p->device);
@@ -577,7 +580,7 @@ int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int dir, const void
   g_launches = 0;
   if (!plans || nplans < 1) return fail(DSFFT_ERR_INVALID, "no plans");
   for (int i = 0; i < nplans; ++i) {
-    int rc = check_exec_args(plans[i], dir, h_in, h_out);
+    int rc = check_exec_args(plans[i], dir, h_in, h_out, batch);
     if (rc) return rc;
     if (plans[i]->n != plans[0]->n || plans[i]->precision != plans[0]->precision ||
         plans[i]->strategy != plans[0]->strategy)
@@ -612,7 +615,7 @@ int dsfft_execute_multi(const dsfft_plan* plans, int nplans, int dir, const void
 int dsfft_error_device(dsfft_plan p, int metric, const void* d_x, size_t batch, void* stream_,
                        dsfft_error_report* out, double* errs_out) {
   g_launches = 0;
-  int rc = check_exec_args(p, DSFFT_FORWARD, d_x, const_cast<void*>(d_x));
+  int rc = check_exec_args(p, DSFFT_FORWARD, d_x, const_cast<void*>(d_x), batch);
   if (rc) return rc;
   if (metric != 0 && metric != 1) return fail(DSFFT_ERR_INVALID, "unknown metric");
   if (batch == 0) return fail(DSFFT_ERR_INVALID, "trials must be >= 1");
@@ -763,7 +766,7 @@ int dsfft_widen(const void* in, double* out, size_t count, int precision) {
 
 int dsfft_execute_f64(dsfft_plan p, int dir, const double* in, double* out, size_t batch) {
   g_launches = 0;
-  int rc = check_exec_args(p, dir, in, out);
+  int rc = check_exec_args(p, dir, in, out, batch);
   if (rc) return rc;
   const size_t count = 2 * p->n * batch;
   std::vector<uint8_t> a(count * (sample_bytes(p->precision) / 2) + 16);

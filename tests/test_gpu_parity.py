@@ -141,6 +141,14 @@ def test_errors(dsfft, cuda):
         dsfft.forward(plan, bad)
     with pytest.raises(ValueError, match="complex128"):
         dsfft.forward(dsfft.make_plan(64, "dual", "fp64"), bad)
+    # raw C ABI: byte-count overflow and misalignment are refused, not launched
+    lib = dsfft._load()
+    buf = cuda.zeros(4096, dtype=cuda.uint8, device="cuda")
+    ptr = buf.data_ptr()
+    assert lib.dsfft_execute(plan._handle, 0, ptr, ptr, 1 << 62, None) == 1
+    assert "overflows" in lib.dsfft_last_error().decode()
+    assert lib.dsfft_execute(plan._handle, 0, ptr + 4, ptr + 4, 1, None) == 1
+    assert "aligned" in lib.dsfft_last_error().decode()
 
 
 @pytest.mark.parametrize("strategy", ALL_STRATEGIES)
