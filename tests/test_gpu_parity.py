@@ -197,6 +197,21 @@ def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
         assert bit_mismatches(y, want) == 0, (n, s, precision)
 
 
+@pytest.mark.parametrize("n,chunk_mb", [(1 << 16, 1), (1 << 20, 5)])
+def test_multipass_in_place(dsfft, cuda, orc, monkeypatch, n, chunk_mb):
+    """in == out through 2- and 3-group splits with odd chunks: a chunk's last
+    group overwrites only input its first group has already consumed."""
+    monkeypatch.setenv("DSFFT_MP_CHUNK_MB", str(chunk_mb))
+    chk = _checker()
+    x = ref_inputs(orc, n, 5, seed=n + 3, precision="fp16")
+    plan = dsfft.make_plan(n, "dual", "fp16")
+    t = cuda.from_numpy(to_work(x, "fp16")).cuda()
+    dsfft.forward(plan, t, out=t)
+    cuda.cuda.synchronize()
+    want = to_work(chk.forward(x, "dual", "fp16"), "fp16")
+    assert bit_mismatches(t.cpu().numpy(), want) == 0
+
+
 @pytest.mark.parametrize("n", [1 << 15, 1 << 17, 1 << 19])
 @pytest.mark.parametrize("precision", ["fp32", "fp16"])
 @pytest.mark.parametrize("strategy", ["standard", "cosine"])
