@@ -13,15 +13,26 @@
 //     counts the reference's kernels would have issued (6 FMAs per butterfly,
 //     4 mul + 6 add for standard, 2n muls for the inverse scaling), since the
 //     hardware FMAs are not routed through the context.
-//   * fp64 plans build their table but forward/inverse throw
-//     std::runtime_error (the device path is fp16/fp32).
+//   * fp64 plans run on the device too (DFMA passes, bit-identical to the
+//     reference's fp64 path).
 //   * Batched overloads (forward_batch / inverse_batch) transform many
 //     SampleBuffers in one call; device-buffer execution is dsfft_execute.
+//   * measure_error runs every trial on the device; its FP64 reference is the
+//     device fp64 transform rather than the O(n^2) dft_oracle (both FP64
+//     accurate; statistics agree to ~1e-9 relative).
+//   * The analysis / serialize surface the CLI uses (table_stats, the bound
+//     tables, write_table_csv, write_bounds_csv, write_error_csv) is mirrored
+//     with byte-identical CSV output.
 #pragma once
 
+#include <bit>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
+#include <numbers>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -268,6 +279,172 @@ inline std::vector<SampleBuffer> inverse_batch(const FftPlan& plan,
                                                const std::vector<SampleBuffer>& spectra,
                                                ArithmeticContext& ctx) {
   return detail::run(plan, spectra, ctx, DSFFT_INVERSE);
+}
+
+// ---- twiddle.hpp: angles and ratio statistics --------------------------------
+// twiddle.cpp:55-57
+inline double twiddle_angle(std::size_t k, std::size_t n) {
+  return -(2.0 * std::numbers::pi) * (static_cast<double>(k) / static_cast<double>(n));
+}
+struct RatioStats {
+  double t_max = 0.0;
+  std::size_t argmax_k = 0;
+  std::size_t singular_count = 0;
+  std::size_t cos_path_count = 0;
+  std::size_t sin_path_count = 0;
+};
+// twiddle.cpp:143-162: clamped entries count as singular and stay out of t_max
+inline RatioStats table_stats(const TwiddleTable& table) {
+  RatioStats s;
+  for (std::size_t k = 0; k < table.entries.size(); ++k) {
+    const TwiddleEntry& e = table.entries[k];
+    (e.path == TwiddlePath::cos ? s.cos_path_count : s.sin_path_count)++;
+    if (e.clamped) {
+      ++s.singular_count;
+      continue;
+    }
+    const double r = std::fabs(e.ratio);
+    if (r > s.t_max) {
+      s.t_max = r;
+      s.argmax_k = k;
+    }
+  }
+  return s;
+}
+
+// ---- analysis.hpp ------------------------------------------------------------
+inline double per_butterfly_bound(double t_max, double eps) { return t_max * eps; }
+inline double cumulative_bound(double t_max, double eps, unsigned m) {
+  return std::pow(1.0 + t_max * eps, static_cast<double>(m)) - 1.0;
+}
+struct BoundReport {
+  Strategy strategy = Strategy::standard;
+  double t_max = 0.0;
+  std::size_t argmax_k = 0;
+  std::size_t singular_count = 0;
+  std::size_t cos_path_count = 0;
+  std::size_t sin_path_count = 0;
+  double per_butterfly_bound = 0.0;
+  double cumulative_bound = 0.0;
+  double improvement_vs_baseline = 1.0;
+  bool divergent = false;
+};
+namespace detail {
+inline BoundReport report_for(const TwiddleTable& table, double eps, unsigned m) {
+  const RatioStats s = table_stats(table);
+  BoundReport r;
+  r.strategy = table.strategy;
+  r.t_max = s.t_max;
+  r.argmax_k = s.argmax_k;
+  r.singular_count = s.singular_count;
+  r.cos_path_count = s.cos_path_count;
+  r.sin_path_count = s.sin_path_count;
+  r.per_butterfly_bound = fmafft_b200::per_butterfly_bound(s.t_max, eps);
+  r.cumulative_bound = fmafft_b200::cumulative_bound(s.t_max, eps, m);
+  r.divergent = r.per_butterfly_bound >= 1.0;
+  return r;
+}
+}  // namespace detail
+// analysis.cpp:65-76: LF, cosine, dual at binary16 epsilon; LF is the baseline
+inline std::vector<BoundReport> reproduce_ratio_table(std::size_t n) {
+  const double eps = machine_epsilon(Precision::fp16);
+  const unsigned m = static_cast<unsigned>(std::countr_zero(n));
+  std::vector<BoundReport> rows{detail::report_for(build_linzer_feig_table(n), eps, m),
+                                detail::report_for(build_cosine_table(n), eps, m),
+                                detail::report_for(build_dual_select_table(n), eps, m)};
+  for (std::size_t i = 1; i < rows.size(); ++i)
+    rows[i].improvement_vs_baseline = rows[0].cumulative_bound / rows[i].cumulative_bound;
+  return rows;
+}
+// analysis.cpp:78-88
+inline std::vector<BoundReport> reproduce_cumulative_table(std::size_t n,
+                                                           Precision precision = Precision::fp16) {
+  const double eps = machine_epsilon(precision);
+  const unsigned m = static_cast<unsigned>(std::countr_zero(n));
+  std::vector<BoundReport> rows{detail::report_for(build_linzer_feig_table(n), eps, m),
+                                detail::report_for(build_dual_select_table(n), eps, m)};
+  rows[1].improvement_vs_baseline = rows[0].cumulative_bound / rows[1].cumulative_bound;
+  return rows;
+}
+
+enum class ErrorMetric { roundtrip, forward_vs_oracle };
+inline std::string_view to_string(ErrorMetric m) {
+  return m == ErrorMetric::roundtrip ? "roundtrip" : "forward_vs_oracle";
+}
+inline ErrorMetric parse_metric(std::string_view name) {
+  if (name == "roundtrip") return ErrorMetric::roundtrip;
+  if (name == "forward" || name == "forward_vs_oracle") return ErrorMetric::forward_vs_oracle;
+  throw std::invalid_argument("unknown metric: " + std::string(name));
+}
+struct ErrorReport {
+  std::size_t n = 0;
+  Strategy strategy = Strategy::standard;
+  Precision precision = Precision::fp64;
+  ErrorMetric metric = ErrorMetric::roundtrip;
+  std::size_t trials = 0;
+  std::uint64_t seed = 0;
+  double rel_l2_median = 0.0;
+  double rel_l2_max = 0.0;
+  std::size_t nonfinite_trials = 0;
+};
+// analysis.hpp:98-100 (the device error harness, dsfft_measure_error)
+inline ErrorReport measure_error(std::size_t n, Strategy strategy, Precision precision,
+                                 ErrorMetric metric, std::size_t trials, std::uint64_t seed,
+                                 int device = 0) {
+  if (trials < 1) throw std::invalid_argument("trials must be >= 1");
+  dsfft_error_report r{};
+  detail::check(dsfft_measure_error(n, int(strategy), int(precision),
+                                    metric == ErrorMetric::roundtrip ? 0 : 1, trials, seed,
+                                    device, &r));
+  ErrorReport e;
+  e.n = n;
+  e.strategy = strategy;
+  e.precision = precision;
+  e.metric = metric;
+  e.trials = trials;
+  e.seed = seed;
+  e.rel_l2_median = r.rel_l2_median;
+  e.rel_l2_max = r.rel_l2_max;
+  e.nonfinite_trials = std::size_t(r.nonfinite_trials);
+  return e;
+}
+
+// ---- serialize.hpp (CSV writers, byte-identical) -------------------------------
+inline std::string format_double(double v) {  // serialize.cpp:42-46
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+// serialize.cpp:48-57
+inline void write_table_csv(std::ostream& os, const TwiddleTable& table) {
+  os << "k,theta,omega_r,omega_i,path,multiplier,ratio,clamped\n";
+  for (std::size_t k = 0; k < table.entries.size(); ++k) {
+    const TwiddleEntry& e = table.entries[k];
+    os << k << ',' << format_double(twiddle_angle(k, table.n)) << ','
+       << format_double(e.omega_r) << ',' << format_double(e.omega_i) << ',' << to_string(e.path)
+       << ',' << format_double(e.multiplier) << ',' << format_double(e.ratio) << ','
+       << (e.clamped ? "true" : "false") << '\n';
+  }
+}
+// serialize.cpp:79-91
+inline void write_bounds_csv(std::ostream& os, const std::vector<BoundReport>& rows) {
+  os << "strategy,t_max,argmax_k,singular_count,cos_path_count,sin_path_count,"
+        "per_butterfly_bound,cumulative_bound,improvement_vs_baseline,divergent\n";
+  for (const BoundReport& r : rows)
+    os << to_string(r.strategy) << ',' << format_double(r.t_max) << ',' << r.argmax_k << ','
+       << r.singular_count << ',' << r.cos_path_count << ',' << r.sin_path_count << ','
+       << format_double(r.per_butterfly_bound) << ',' << format_double(r.cumulative_bound)
+       << ',' << format_double(r.improvement_vs_baseline) << ','
+       << (r.divergent ? "true" : "false") << '\n';
+}
+// serialize.hpp:33-35 schema: n,strategy,precision,metric,trials,seed,rel_l2_median,
+// rel_l2_max,nonfinite_trials
+inline void write_error_csv(std::ostream& os, const ErrorReport& r) {
+  os << "n,strategy,precision,metric,trials,seed,rel_l2_median,rel_l2_max,nonfinite_trials\n"
+     << r.n << ',' << to_string(r.strategy) << ',' << to_string(r.precision) << ','
+     << to_string(r.metric) << ',' << r.trials << ',' << r.seed << ','
+     << format_double(r.rel_l2_median) << ',' << format_double(r.rel_l2_max) << ','
+     << r.nonfinite_trials << '\n';
 }
 
 }  // namespace fmafft_b200

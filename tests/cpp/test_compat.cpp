@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 
 #include "fmafft_b200.hpp"
@@ -106,6 +107,29 @@ static void host_checks() {
 }
 
 static void device_checks() {
+  // acceptance.cpp:209-242 / test_analysis.cpp:144-172 through measure_error:
+  // fp16 dual beats LF with the clamp, within the paper's cumulative bound
+  {
+    const ErrorReport d =
+        measure_error(1024, Strategy::dual_select, Precision::fp16, ErrorMetric::forward_vs_oracle,
+                      10, 42);
+    const ErrorReport lf =
+        measure_error(1024, Strategy::linzer_feig, Precision::fp16, ErrorMetric::forward_vs_oracle,
+                      10, 42);
+    CHECK(d.trials == 10 && d.nonfinite_trials == 0 && lf.nonfinite_trials == 0);
+    CHECK(d.rel_l2_median < lf.rel_l2_median);
+    CHECK(d.rel_l2_max <= reproduce_cumulative_table(1024)[1].cumulative_bound);
+    const ErrorReport rt = measure_error(1024, Strategy::dual_select, Precision::fp32,
+                                         ErrorMetric::roundtrip, 20, 42);
+    CHECK(rt.rel_l2_median > 1e-8 && rt.rel_l2_median < 1e-6);  // acceptance.cpp:185-205
+    std::ostringstream os;
+    write_error_csv(os, rt);
+    CHECK(os.str().rfind("n,strategy,precision,metric,trials,seed,", 0) == 0);
+    CHECK(os.str().find("\n1024,dual,fp32,roundtrip,20,42,") != std::string::npos);
+    CHECK_THROWS_AS(measure_error(64, Strategy::dual_select, Precision::fp16,
+                                  ErrorMetric::roundtrip, 0, 1),
+                    std::invalid_argument);
+  }
   // test_fft.cpp:33-61 plan construction and table rounding
   const FftPlan p = make_plan(1024, Strategy::dual_select, Precision::fp16);
   CHECK(p.n == 1024 && p.m == 10 && p.table.entries.size() == 512);
@@ -217,7 +241,45 @@ static void device_checks() {
   }
 }
 
+// `test_compat csv`: the CLI's table and statistics dumps through the C++
+// mirror (write_table_csv of build_table, write_bounds_csv of the bound
+// tables), compared byte for byte with the reference's own dumps by
+// tests/test_cpp_compat.py.
+static int csv_dump() {
+  std::ostringstream os;
+  const struct {
+    std::size_t n;
+    Strategy s;
+    const char* name;
+  } tables[] = {{64, Strategy::dual_select, "dual"},
+                {64, Strategy::linzer_feig, "lf"},
+                {8, Strategy::standard, "standard"}};
+  for (const auto& t : tables) {
+    os << "== csv/" << t.n << "/" << t.name << "/fp64\n";
+    write_table_csv(os, build_table(t.n, t.s));
+  }
+  for (std::size_t n : {std::size_t(1024), std::size_t(64), std::size_t(1) << 20, std::size_t(2)}) {
+    os << "== bounds/" << n << "/stats/fp16\n";
+    write_bounds_csv(os, reproduce_ratio_table(n));
+  }
+  const struct {
+    std::size_t n;
+    Precision p;
+    const char* name;
+  } cum[] = {{1024, Precision::fp16, "fp16"},
+             {1024, Precision::fp32, "fp32"},
+             {4096, Precision::fp64, "fp64"},
+             {8, Precision::fp16, "fp16"}};
+  for (const auto& c : cum) {
+    os << "== bounds/" << c.n << "/bounds/" << c.name << "\n";
+    write_bounds_csv(os, reproduce_cumulative_table(c.n, c.p));
+  }
+  std::fputs(os.str().c_str(), stdout);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::strcmp(argv[1], "csv") == 0) return csv_dump();
   host_checks();
   if (!(argc > 1 && std::strcmp(argv[1], "host") == 0)) device_checks();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);

@@ -23,6 +23,19 @@ def test_cpp_dropin_host(exe):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+def test_cpp_csv_dumps_match_reference(exe):
+    """write_table_csv / write_bounds_csv through the C++ mirror == the
+    reference's own serializer output (golden dumps), byte for byte."""
+    import numpy as np
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))
+    r = subprocess.run([exe, "csv"], capture_output=True, text=True, check=True)
+    parts = r.stdout.split("== ")[1:]
+    assert len(parts) == 11
+    for part in parts:
+        key, body = part.split("\n", 1)
+        assert body.encode() == g[key].tobytes(), key
+
+
 @pytest.mark.gpu
 def test_cpp_dropin_device(exe, cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
