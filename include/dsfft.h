@@ -49,7 +49,7 @@ typedef enum { DSFFT_FORWARD = 0, DSFFT_INVERSE = 1 } dsfft_direction;
 typedef enum {
   DSFFT_OK = 0,
   DSFFT_ERR_INVALID = 1,     /* reference: std::invalid_argument */
-  DSFFT_ERR_UNSUPPORTED = 2, /* valid for the reference, not on this device path */
+  DSFFT_ERR_UNSUPPORTED = 2, /* reserved: every reference configuration runs on the device */
   DSFFT_ERR_CUDA = 3,        /* CUDA runtime / launch failure */
   DSFFT_ERR_NO_DEVICE = 4    /* no sm_100 device: the product never falls back to CPU */
 } dsfft_status;
