@@ -12,8 +12,18 @@
 namespace dsfft {
 
 //            LOG_N LOG_E W  stages (passes per register stage)
-#if DSFFT_M <= 5
-using CfgW = Sched<DSFFT_M, 5, 1, DSFFT_M>;
+#if DSFFT_M == 1
+using CfgW = Sched<1, 5, 1, 1>;
+using CfgC = CfgW;
+#elif DSFFT_M <= 5
+// A single register stage would have lane t read (and store) values t*32..:
+// stride-N lanes, 32-way shared-memory conflicts and uncoalesced stores
+// (schedule_check: 1024/32 load wavefronts at N=32).  Splitting off one-pass
+// stages at both ends keeps the TMA tile reads and the global stores
+// lane-contiguous (64/32) at the cost of two padded exchanges.
+using CfgW = std::conditional_t<DSFFT_M == 2, Sched<2, 5, 1, 1, 1>,
+             std::conditional_t<DSFFT_M == 3, Sched<3, 5, 1, 1, 1, 1>,
+             std::conditional_t<DSFFT_M == 4, Sched<4, 5, 1, 1, 2, 1>, Sched<5, 5, 1, 1, 3, 1>>>>;
 using CfgC = CfgW;
 #elif DSFFT_M == 6
 using CfgW = Sched<6, 5, 1, 3, 3>;
