@@ -518,16 +518,17 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
                         cudaStream_t st) {
   using Lay = MpLayout<S1, A>;
   MpParams q = p;
-  // ring depth S and tile groups per CTA G.  First groups (tiny twiddle
-  // table) run one group per CTA and several CTAs per SM; later groups share
-  // one column-block slab between G groups of one CTA (<= 512 threads).
+  // ring depth S and tile groups per CTA G (later groups share one
+  // column-block slab between their G groups; <= 512 threads).  Default: two
+  // independent groups, giving up ring depth before groups when shared memory
+  // is short -- two 1-deep groups beat one 2-deep group by 0-3% (B200 sweep).
   const char* es = std::getenv("DSFFT_MP_STAGES");
   const char* eg = std::getenv("DSFFT_MP_GROUPS");
   int stages = es && *es ? std::max(1, std::atoi(es)) : 2;
-  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : (first ? 1 : std::max(1, 512 / Lay::T));
+  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : 2;
   groups = std::min(groups, std::max(1, 512 / Lay::T));
-  while (groups > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --groups;
   while (stages > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --stages;
+  while (groups > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --groups;
   q.stages = stages;
   const size_t smem = Lay::smem_bytes(first, stages, groups);
   const int threads = groups * Lay::T;
