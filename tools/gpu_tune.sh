@@ -13,8 +13,11 @@
 #     DSFFT_MP_STAGES     ring depth;  DSFFT_MP_GROUPS  tile groups per CTA
 #     DSFFT_MP_CHUNK_MB   batch chunk per launch sequence
 #     DSFFT_MP_F16_LAYOUT 1 = transform pairs, 2 = one complex per register
+#     DSFFT_MP_SPLIT      pass-group sizes, e.g. "9,7" (each 6..9, summing to log2 N)
 #   host pipeline
 #     DSFFT_HOST_CHUNK_MB chunk of dsfft_execute_host's H2D/kernel/D2H pipeline
+#   A/B builds
+#     DSFFT_LIBRARY       path of another libdsfft.so build to load instead
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 N=${N:-1024}
