@@ -23,8 +23,10 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["Strategy", "Precision", "FftPlan", "make_plan", "forward", "inverse",
-           "execute", "forward_f64", "inverse_f64", "execute_host", "round_to", "widen",
-           "parse_strategy", "parse_precision", "library_path", "DsfftError"]
+           "execute", "forward_f64", "inverse_f64", "execute_host", "execute_multi",
+           "round_to", "widen", "build_table", "table_csv", "bounds_csv", "error_device",
+           "measure_error", "last_launch_count", "parse_strategy", "parse_precision",
+           "library_path", "DsfftError"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # DSFFT_LIBRARY: load another build of the library (A/B timing of two builds)
@@ -256,9 +258,19 @@ def inverse(plan: FftPlan, x, out=None, stream=None):
     return execute(plan, 1, x, out, stream)
 
 
+def _check_host(plan: FftPlan, h_in: np.ndarray, h_out: np.ndarray, batch: int) -> None:
+    need = int(batch) * plan.n * sample_bytes(plan.precision)
+    if h_in.nbytes < need or h_out.nbytes < need:
+        raise ValueError(f"host buffers hold {h_in.nbytes} / {h_out.nbytes} bytes, "
+                         f"batch {batch} needs {need}")
+    if not (h_in.flags.c_contiguous and h_out.flags.c_contiguous):
+        raise ValueError("host buffers must be C-contiguous")
+
+
 def execute_host(plan: FftPlan, direction: int, h_in: np.ndarray, h_out: np.ndarray,
                  batch: int, stream: int = 0) -> None:
     """Host buffers in the working precision (pinned for full overlap)."""
+    _check_host(plan, h_in, h_out, batch)
     _check(_load().dsfft_execute_host(plan._handle, direction, h_in.ctypes.data,
                                       h_out.ctypes.data, batch, stream))
 
@@ -310,6 +322,9 @@ def execute_multi(plans, direction: int, h_in: np.ndarray, h_out: np.ndarray,
                   batch: int) -> None:
     """Batch partitioner over devices (dsfft_execute_multi): plans[i] runs the
     contiguous shard i of the host batch on its own device."""
+    if not plans:
+        raise ValueError("no plans")
+    _check_host(plans[0], h_in, h_out, batch)
     lib = _load()
     lib.dsfft_execute_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                         C.c_size_t]
