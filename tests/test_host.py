@@ -57,6 +57,22 @@ def test_host_tables_match_reference(dsfft, ref):
                 assert dsfft.build_table(n, s, p).tobytes() == ref.plan_table(n, s, p).tobytes()
 
 
+def test_lf_clamp_eps_matches_reference(dsfft, ref):
+    """build_table(n, linzer_feig, clamp_eps) (twiddle.cpp:74-95) for non-default
+    clamps, incl. values that round to zero / subnormal in binary16."""
+    for eps in (1e-3, 1e-5, 2.0 ** -24, 1e-9, 1e-12, 0.5):
+        for n in (2, 16, 1024):
+            got = dsfft.build_table(n, "lf", "fp64", clamp_eps=eps)
+            want = ref.build_table(n, "lf", clamp_eps=eps)
+            assert got.tobytes() == want.tobytes(), (eps, n)
+            for p in ("fp16", "fp32"):  # the rounded entries, eps rounded once
+                g = dsfft.build_table(n, "lf", p, clamp_eps=eps)
+                w = want.copy()
+                for f in ("multiplier", "ratio", "omega_r", "omega_i"):
+                    w[f] = dsfft.widen(dsfft.round_to(want[f], p), p)
+                assert g.tobytes() == w.tobytes(), (eps, n, p)
+
+
 def test_table_csv_matches_reference_writer(dsfft):
     """dsfft_table_csv == the reference's write_table_csv (serialize.cpp:48-57),
     byte for byte (golden dumps produced by the reference's own serializer)."""
