@@ -126,9 +126,10 @@ def _check(rc: int) -> None:
     raise DsfftError(msg)
 
 
-@dataclass
+@dataclass(eq=False)
 class FftPlan:
-    """Mirror of fmafft::FftPlan (fft.hpp:17-23) owning a device plan."""
+    """Mirror of fmafft::FftPlan (fft.hpp:17-23) owning a device plan (the
+    handle is destroyed with the object; plans are shareable, not copyable)."""
     n: int
     m: int
     strategy: str
@@ -142,6 +143,10 @@ class FftPlan:
         out = np.zeros(max(self.n // 2, 1), dtype=ENTRY_DTYPE)
         _check(_load().dsfft_plan_table(self._handle, out.ctypes.data, out.size))
         return out[: self.n // 2]
+
+    def __reduce_ex__(self, protocol):
+        raise TypeError("FftPlan owns a device plan and cannot be copied or pickled; "
+                        "share the object or call make_plan again")
 
     def __del__(self):
         h = getattr(self, "_handle", None)
