@@ -76,7 +76,8 @@ struct MpLayout {
   static constexpr int kTileBytes = 32 * L * VB;
   // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned
   // later groups keep their column block's whole twiddle slab in smem (stage 1
-  // and 2) when it fits next to the ring (S1 <= 3: <= 130 KB); S1 = 4 stages
+  // and 2) when it fits next to the ring (S1 <= 3: <= 65 KB with 8-byte fp16 pair
+  // records, 130 KB with 16-byte records); S1 = 4 stages
   // only the stage-1 part and reads stage 2 through L1
   static constexpr bool kFullSlab = S1 <= 3;
   static constexpr int kSlabRecords = kFullSlab ? mp_block_records(S1) : 31 * 32;

@@ -66,7 +66,7 @@ DSFFT_HD constexpr int tw_entry(int m, int P, int r, int pl, int rl) {
 }
 
 // Slot of that twiddle in the per-stage device table: consecutive r are
-// adjacent so lanes with consecutive groups read consecutive 16-byte records.
+// adjacent so lanes with consecutive groups read consecutive records (8 or 16 B).
 DSFFT_HD constexpr int tw_slot(int P, int r, int pl, int rl) {
   return (((1 << pl) - 1 + rl) << P) + r;
 }
@@ -92,7 +92,7 @@ struct Sched {
   DSFFT_HD static constexpr int P(int i) {
     return i == 0 ? 0 : i == 1 ? S0 : i == 2 ? S0 + S1 : S0 + S1 + S2;
   }
-  // Twiddle table offsets (in 16-byte records) of each stage.
+  // Twiddle table offsets (in records) of each stage.
   DSFFT_HD static constexpr int tw_off(int i) {
     int off = 0;
     for (int k = 0; k < i; ++k) off += tw_stage_size(P(k), s(k));
