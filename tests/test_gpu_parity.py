@@ -166,6 +166,19 @@ def test_fp64_bit_exact(dsfft, cuda, orc, n, strategy, inverse):
     assert bit_mismatches(y.view(np.float64), want.view(np.float64)) == 0
 
 
+@pytest.mark.parametrize("m", [18, 20, 24])
+def test_fp64_large_n(dsfft, cuda, orc, m):
+    """fp64 per-pass kernels up to the 2^24 cap: bit-exact vs the reference."""
+    chk = _checker()
+    n = 1 << m
+    x = orc.random_buffer(n, 7 + m, batch=1)
+    t = cuda.from_numpy(np.ascontiguousarray(x)).cuda()
+    for inverse in (False, True):
+        y = dsfft.execute(dsfft.make_plan(n, "dual", "fp64"), int(inverse), t).cpu().numpy()
+        want = (chk.inverse if inverse else chk.forward)(x, "dual", "fp64")
+        assert bit_mismatches(y.view(np.float64), want.view(np.float64)) == 0, (m, inverse)
+
+
 def test_fp64_oracle_equivalence(dsfft, cuda, orc):
     """test_fft.cpp:110-128 / acceptance criterion 5 through the device:
     every strategy within rel-L2 1e-11 of the FP64 DFT, n <= 4096."""
