@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-ffp-contract=off", f"-I{ROOT}/include", f"-I{CSRC}"]
-SMALL_SIZES = range(1, 13)
+SMALL_SIZES = range(1, 14)
 
 
 def _headers():

@@ -57,12 +57,13 @@ struct DeviceGuard {
 };
 
 const dsfft::SmallEntry& small_entry(int m) {
-  static const dsfft::SmallEntry table[13] = {
+  static const dsfft::SmallEntry table[14] = {
       {},
       dsfft::small_entry_m1(),  dsfft::small_entry_m2(),  dsfft::small_entry_m3(),
       dsfft::small_entry_m4(),  dsfft::small_entry_m5(),  dsfft::small_entry_m6(),
       dsfft::small_entry_m7(),  dsfft::small_entry_m8(),  dsfft::small_entry_m9(),
-      dsfft::small_entry_m10(), dsfft::small_entry_m11(), dsfft::small_entry_m12()};
+      dsfft::small_entry_m10(), dsfft::small_entry_m11(), dsfft::small_entry_m12(),
+      dsfft::small_entry_m13()};
   return table[m];
 }
 
@@ -327,7 +328,7 @@ int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, i
   if (precision == DSFFT_FP64) {
     p->f64 = dsfft::fp64_create(p->table, int(p->m), strategy);
     if (!p->f64) rc = fail(DSFFT_ERR_CUDA, dsfft::fp64_error());
-  } else if (p->m <= 12) {
+  } else if (p->m <= 12 || (p->m == 13 && env_int("DSFFT_SMALL13", 1) != 0)) {
     const dsfft::SmallEntry& se = small_entry(int(p->m));
     p->variant = dsfft::kVarF32;
     if (precision == DSFFT_FP16) {

@@ -49,8 +49,13 @@ using CfgC = Sched<11, 6, 1, 5, 6>;
 #elif DSFFT_M == 12
 using CfgW = Sched<12, 5, 4, 5, 5, 2>;
 using CfgC = Sched<12, 6, 2, 6, 6>;
+#elif DSFFT_M == 13
+// 8 warps per item, conflict-free for every value width (schedule_check);
+// fp16 pairs: 64 KB of 8-byte records + two 66 KB items per SM
+using CfgW = Sched<13, 5, 8, 5, 5, 3>;
+using CfgC = CfgW;
 #else
-#error "single-kernel path covers N <= 4096"
+#error "single-kernel path covers N <= 8192"
 #endif
 
 #define DSFFT_CAT2(a, b) a##b

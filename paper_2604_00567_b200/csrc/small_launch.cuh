@@ -107,5 +107,6 @@ SmallEntry small_entry_m9();
 SmallEntry small_entry_m10();
 SmallEntry small_entry_m11();
 SmallEntry small_entry_m12();
+SmallEntry small_entry_m13();
 
 }  // namespace dsfft
