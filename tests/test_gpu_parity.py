@@ -210,6 +210,21 @@ def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
         assert bit_mismatches(y, want) == 0, (n, s, precision)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_multipass_at_8192(dsfft, cuda, orc, monkeypatch, precision):
+    """N=8192 runs in the single kernel by default; its two-launch path
+    (DSFFT_SMALL13=0) stays bit-exact too."""
+    monkeypatch.setenv("DSFFT_SMALL13", "0")
+    chk = _checker()
+    x = ref_inputs(orc, 8192, 5, seed=8192 + 5, precision=precision)
+    for inverse in (False, True):
+        plan = dsfft.make_plan(8192, "dual", precision)
+        y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+        want = to_work((chk.inverse if inverse else chk.forward)(x, "dual", precision), precision)
+        assert bit_mismatches(y, want) == 0, (precision, inverse)
+        assert dsfft.last_launch_count() == 2
+
+
 @pytest.mark.parametrize("n,chunk_mb", [(1 << 16, 1), (1 << 20, 5)])
 def test_multipass_in_place(dsfft, cuda, orc, monkeypatch, n, chunk_mb):
     """in == out through 2- and 3-group splits with odd chunks: a chunk's last
