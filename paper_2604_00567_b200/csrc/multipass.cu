@@ -1,4 +1,4 @@
-// multipass.cu -- batched forward/inverse for N = 2^13 .. 2^24.
+// multipass.cu -- batched forward/inverse for N = 2^14 .. 2^24 (and 2^13 on request).
 //
 // The m = log2 N passes are split into 2-3 consecutive pass groups
 // [P, P+s), s in 6..9, each one launch of mp_kernel (SURVEY.md A.1 item 3
