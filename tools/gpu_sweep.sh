@@ -6,13 +6,15 @@ cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 out=gpurun_out/sweep.jsonl
 : > "$out"
-NS=${NS:-"64 128 256 512 1024 2048 4096"}
-LARGE=${LARGE:-"8192 65536 262144 1048576 16777216"}
+NS=${NS:-"64 128 256 512 1024 2048 4096 8192"}
+LARGE=${LARGE:-"16384 65536 262144 1048576 16777216"}
 for n in $NS; do
   for p in fp16 fp32; do
+    sb=$([ "$p" = fp16 ] && echo 4 || echo 8)
+    batch=$(( (4 << 30) / (n * sb) ))  # >= 4 GiB of input
     for s in ${STRATS:-standard lf cosine dual}; do
       timeout 300 python bench.py --n "$n" --precision "$p" --strategy "$s" --steps "${STEPS:-30}" \
-        --warmup 3 --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
+        --warmup 3 --batch "$batch" --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
     done
   done
 done
