@@ -18,8 +18,10 @@ Reported on rank 0 as one JSON line: value = transforms/s of the whole job,
 roofline (HBM bytes = 2*N*sizeof(complex) per transform vs the measured copy
 bandwidth in MEASURED_PEAKS.json), e2e through the C ABI with pinned host
 buffers (dsfft_execute_host: H2D + kernels + D2H inside the timed region),
-accuracy vs an FP64 DFT on a sample, cpu_baseline (the reference's own CPU
-path, oracle/_ref, on this host's cores), clocks sampled during the run.
+accuracy of every transform of the batch vs an FP64 reference transform on the
+device (plus the LF comparison and the paper's bound), cpu_baseline (the
+reference's own CPU path, oracle/_ref, on this host's cores), clocks sampled
+during the run.
 """
 from __future__ import annotations
 
