@@ -122,10 +122,12 @@ template <class A>
 __host__ __device__ constexpr int value_bytes() { return A::kWords * 4; }
 
 // CTA size cap (sets the register budget): 2E data registers for two-word
-// values (E=32 -> 128 regs, 512 threads), E for one-word values.
+// values (E=32 -> 128 regs, 512 threads; E=16 -> ~80 regs, 768 threads), E for
+// one-word values.
 template <class Cfg, class A>
 __host__ __device__ constexpr int max_threads() {
-  return A::kWords == 2 ? (Cfg::LOG_E >= 6 ? 256 : 512) : (Cfg::LOG_E >= 6 ? 512 : 768);
+  return A::kWords == 2 ? (Cfg::LOG_E >= 6 ? 256 : Cfg::LOG_E <= 4 ? 768 : 512)
+                        : (Cfg::LOG_E >= 6 ? 512 : 768);
 }
 
 // One radix-2 butterfly, A = a + W b, B = a - W b.

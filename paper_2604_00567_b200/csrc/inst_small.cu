@@ -58,11 +58,20 @@ using CfgC = CfgW;
 #error "single-kernel path covers N <= 8192"
 #endif
 
+// fp32 at N = 256 / 512: 16 values per thread (E=16, ~80 registers) and more
+// resident warps beat E=32 (B200 sweep at >= 4 GiB per step: +2% / +4%)
+#if DSFFT_M == 8
+using CfgF = Sched<8, 4, 1, 4, 4>;
+#elif DSFFT_M == 9
+using CfgF = Sched<9, 4, 1, 4, 4, 1>;
+#else
+using CfgF = CfgW;
+#endif
 #define DSFFT_CAT2(a, b) a##b
 #define DSFFT_CAT(a, b) DSFFT_CAT2(a, b)
 SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   SmallEntry e{};
-  e.v[kVarF32] = make_variant<CfgW, ArithF32>();
+  e.v[kVarF32] = make_variant<CfgF, ArithF32>();
   e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
   e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
   // Defaults from B200 sweeps (profiles/README.md, "launch shapes"):
@@ -71,7 +80,7 @@ SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   // shared-memory bound (per-stage twiddle tables ~N*8 B plus 32 KB items),
   // where a 1-deep ring with more groups wins.
   e.f16_default = DSFFT_M >= 8 ? kVarF16P : kVarF16C;
-  e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : 3;
+  e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : DSFFT_M == 8 ? 4 : DSFFT_M == 9 ? 2 : 3;
   e.stages[kVarF16P] = DSFFT_M >= 11 ? 1 : 2;
   e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : 2;
   return e;
