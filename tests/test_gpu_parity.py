@@ -10,7 +10,7 @@ or the reference library itself when oracle/_ref was built.
 import numpy as np
 import pytest
 
-from helpers import ALL_STRATEGIES, WORK_DTYPE, bit_mismatches, max_ulp_fp16, ref_inputs, to_work
+from helpers import ALL_STRATEGIES, bit_mismatches, max_ulp_fp16, ref_inputs, to_work
 
 pytestmark = pytest.mark.gpu
 
