@@ -347,3 +347,28 @@ def test_execute_multi_partitioner(dsfft, cuda, orc):
     want = to_work(_checker().forward(ref_inputs(orc, n, batch, 21, "fp16"), "dual", "fp16"),
                    "fp16")
     assert bit_mismatches(out, want) == 0
+
+
+def test_plan_lifecycle_releases_device_memory(dsfft, cuda):
+    """Creating and destroying plans of every path (single kernel, multipass,
+    fp64, host pipeline) returns their device memory."""
+    import gc
+    import numpy as np
+
+    def cycle():
+        for n, p in ((1024, "fp16"), (4096, "fp32"), (1 << 16, "fp16"), (1 << 20, "fp32"),
+                     (256, "fp64")):
+            plan = dsfft.make_plan(n, "dual", p)
+            if p != "fp64":
+                xw = np.zeros((2, n, 2), dtype=np.float16 if p == "fp16" else np.float32)
+                dsfft.execute_host(plan, 0, xw, np.empty_like(xw), 2)
+            del plan
+        gc.collect()
+        cuda.cuda.synchronize()
+
+    cycle()  # first use: module loads, pools, cuBLAS-free context setup
+    free0, _ = cuda.cuda.mem_get_info()
+    for _ in range(5):
+        cycle()
+    free1, _ = cuda.cuda.mem_get_info()
+    assert free0 - free1 < (64 << 20), (free0, free1)
