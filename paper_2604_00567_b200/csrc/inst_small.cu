@@ -75,14 +75,15 @@ SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
   e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
   // Defaults from B200 sweeps (profiles/README.md, "launch shapes"):
-  // with 8-byte records, fp16 transform pairs win from N = 256 (97% of HBM vs
-  // 87% one-complex) up; one complex per register for N <= 128.  N >= 2048 is
+  // with 8-byte records, fp16 transform pairs win from N = 128 (95-97% of HBM
+  // with a 1-deep ring vs 92% one-complex) up; one complex per register (3-deep
+  // ring at N = 64) below.  N >= 2048 is
   // shared-memory bound (per-stage twiddle tables ~N*8 B plus 32 KB items),
   // where a 1-deep ring with more groups wins.
-  e.f16_default = DSFFT_M >= 8 ? kVarF16P : kVarF16C;
+  e.f16_default = DSFFT_M >= 7 ? kVarF16P : kVarF16C;
   e.stages[kVarF32] = DSFFT_M >= 11 ? 1 : DSFFT_M == 8 ? 4 : DSFFT_M == 9 ? 2 : 3;
-  e.stages[kVarF16P] = DSFFT_M >= 11 ? 1 : 2;
-  e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : 2;
+  e.stages[kVarF16P] = (DSFFT_M >= 11 || DSFFT_M == 7) ? 1 : 2;  // N=128: 1-deep, 16 groups
+  e.stages[kVarF16C] = DSFFT_M >= 11 ? 1 : DSFFT_M == 6 ? 3 : 2;
   return e;
 }
 
