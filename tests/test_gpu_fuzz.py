@@ -1,6 +1,8 @@
 """Randomised GPU parity (seeded): random sizes, strategies, precisions,
 directions, odd batches, in-place or not -- every case bit-exact against the
 reference (or the oracle).  Plus CUDA-graph capture of dsfft_execute."""
+import os
+
 import numpy as np
 import pytest
 
@@ -14,10 +16,15 @@ def _checker():
     return oracle.load_ref() if oracle.ref_available() else oracle.load_oracle()
 
 
-@pytest.mark.parametrize("case", range(40))
+# DSFFT_FUZZ_CASES / DSFFT_FUZZ_SEED widen the sweep for soak runs
+_CASES = int(os.environ.get("DSFFT_FUZZ_CASES", "40"))
+_SEED = int(os.environ.get("DSFFT_FUZZ_SEED", "1234"))
+
+
+@pytest.mark.parametrize("case", range(_CASES))
 def test_random_cases(dsfft, cuda, orc, case):
     torch = cuda
-    rng = np.random.RandomState(1234 + case)
+    rng = np.random.RandomState(_SEED + case)
     m = int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]))
     n = 1 << m
     precision = str(rng.choice(["fp16", "fp32", "fp64"]))
