@@ -19,13 +19,14 @@ def _checker():
 # DSFFT_FUZZ_CASES / DSFFT_FUZZ_SEED widen the sweep for soak runs
 _CASES = int(os.environ.get("DSFFT_FUZZ_CASES", "40"))
 _SEED = int(os.environ.get("DSFFT_FUZZ_SEED", "1234"))
+_MAXM = int(os.environ.get("DSFFT_FUZZ_MAXM", "15"))
 
 
 @pytest.mark.parametrize("case", range(_CASES))
 def test_random_cases(dsfft, cuda, orc, case):
     torch = cuda
     rng = np.random.RandomState(_SEED + case)
-    m = int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]))
+    m = int(rng.choice(list(range(1, 16)) + list(range(16, _MAXM + 1))))
     n = 1 << m
     precision = str(rng.choice(["fp16", "fp32", "fp64"]))
     strategy = str(rng.choice(ALL_STRATEGIES))
