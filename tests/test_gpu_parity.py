@@ -372,3 +372,66 @@ def test_plan_lifecycle_releases_device_memory(dsfft, cuda):
         cycle()
     free1, _ = cuda.cuda.mem_get_info()
     assert free0 - free1 < (64 << 20), (free0, free1)
+
+
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_headline_size_properties(dsfft, cuda, orc, precision):
+    """BASELINE configs[1] at full size (N=1024, batch 2^20 fp16 / 2^19 fp32):
+    64 sampled transforms bit-exact against the reference, the impulse maps to
+    exact ones, and the round trip of every transform stays within the
+    reference's fp32 window / the fp16 cumulative bound (analysis.cpp:61-63)."""
+    torch = cuda
+    n = 1024
+    batch = (1 << 20) if precision == "fp16" else (1 << 19)
+    wdt = torch.float16 if precision == "fp16" else torch.float32
+    g = torch.Generator(device="cuda")
+    g.manual_seed(99)
+    x = (torch.rand((batch, n, 2), device="cuda", generator=g) * 2 - 1).to(wdt)
+    x[7] = 0
+    x[7, 0, 0] = 1  # impulse
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = dsfft.forward(plan, x)
+    torch.cuda.synchronize()
+    idx = torch.randint(0, batch, (64,), generator=g, device="cuda").cpu().numpy()
+    xs = x[idx].float().cpu().numpy().astype(np.float64)
+    xs = (xs[..., 0] + 1j * xs[..., 1]).astype(np.complex128)
+    want = to_work(_checker().forward(xs, "dual", precision), precision)
+    assert bit_mismatches(y[idx].cpu().numpy(), want) == 0
+    imp = y[7].float().cpu().numpy()
+    assert (imp[:, 0] == 1).all() and (imp[:, 1] == 0).all()
+    rep = dsfft.error_device(plan, x, "roundtrip")
+    assert rep["trials"] == batch and rep["nonfinite_trials"] == 0
+    if precision == "fp32":
+        assert 1e-8 < rep["rel_l2_median"] < 1e-6  # acceptance.cpp:185-205
+    else:
+        assert rep["rel_l2_max"] < 2 * 0.0048935553178424129  # forward + inverse bound
+
+
+@pytest.mark.parametrize("n,precision,sample", [(1 << 16, "fp16", 4), (1 << 20, "fp32", 2)])
+def test_config5_size_properties(dsfft, cuda, orc, n, precision, sample):
+    """BASELINE configs[4] sizes at a full 1 GiB batch: sampled transforms
+    bit-exact against the reference and every transform's round trip finite
+    and small (multipass path)."""
+    torch = cuda
+    sb = 4 if precision == "fp16" else 8
+    batch = (1 << 30) // (n * sb)
+    wdt = torch.float16 if precision == "fp16" else torch.float32
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = (torch.rand((batch, n, 2), device="cuda", generator=g) * 2 - 1).to(wdt)
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = dsfft.forward(plan, x)
+    torch.cuda.synchronize()
+    idx = np.array([0, batch - 1] + list(range(1, batch - 1, max(1, batch // sample))))[:sample]
+    xs = x[idx].float().cpu().numpy().astype(np.float64)
+    xs = (xs[..., 0] + 1j * xs[..., 1]).astype(np.complex128)
+    want = to_work(_checker().forward(xs, "dual", precision), precision)
+    assert bit_mismatches(y[idx].cpu().numpy(), want) == 0
+    # fp16 at 2^16: the reference's inverse scales after the transform
+    # (fft.cpp:86-101), so an unscaled N*x overflows binary16 and the round trip
+    # is non-finite by construction -- check the forward error instead, within
+    # the paper's cumulative bound (1 + 2^-11)^16 - 1 (analysis.cpp:61-63)
+    metric = "roundtrip" if precision == "fp32" else "forward"
+    rep = dsfft.error_device(plan, x, metric)
+    assert rep["trials"] == batch and rep["nonfinite_trials"] == 0
+    assert rep["rel_l2_max"] < (5e-6 if precision == "fp32" else (1 + 2.0 ** -11) ** 16 - 1)
