@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DSFFT_VERSION 1
+#define DSFFT_VERSION 2
 
 typedef enum {
   DSFFT_STANDARD = 0,
@@ -74,6 +74,16 @@ typedef struct {
  * n: power of two in [2, 2^24]; clamp_eps > 0 (used by linzer_feig only). */
 int dsfft_plan_create(size_t n, int strategy, int precision, double clamp_eps, int device,
                       dsfft_plan* out);
+
+/* A plan over a caller-supplied table: `table` holds the n/2 records of
+ * FftPlan::table.entries exactly as the reference's forward would read them
+ * (already rounded into `precision`, possibly edited by the caller -- the
+ * reference's FftPlan is a plain struct with a public table, see the
+ * "negative control" case of test_fft.cpp).  Records are packed and uploaded
+ * as given; nothing is recomputed.  strategy selects the butterfly
+ * (butterfly.cpp:82-90 kernel_for). */
+int dsfft_plan_create_with_table(size_t n, int strategy, int precision, const dsfft_entry* table,
+                                 size_t count, int device, dsfft_plan* out);
 
 int dsfft_plan_destroy(dsfft_plan plan);
 
@@ -161,22 +171,57 @@ typedef struct {
   uint64_t nonfinite_trials;
 } dsfft_error_report;
 
+/* FP64 reference of the forward_vs_oracle metric:
+ *   DSFFT_REF_DFT    the device dft_oracle (bit-identical to fft.cpp:103-121;
+ *                    O(n^2) per transform);
+ *   DSFFT_REF_FFT64  this library's fp64 FFT (bit-identical to the
+ *                    reference's fp64 forward; within 1e-11 of the DFT);
+ *   DSFFT_REF_AUTO   the DFT for n <= 4096, the fp64 FFT above. */
+enum { DSFFT_REF_AUTO = 0, DSFFT_REF_DFT = 1, DSFFT_REF_FFT64 = 2 };
+
 /* Device error harness over a whole batch already on the device (working
- * precision): per-transform relative_l2_error (analysis.cpp:41-57) of the
- * forward against an FP64 reference transform, or of inverse(forward(x))
- * against x; median over finite transforms, max (+inf if any non-finite) and
- * the non-finite count (analysis.cpp:16-22,142-152).  `errs` (optional,
- * `batch` doubles, host) receives the per-transform errors. */
+ * precision, 16-byte aligned): per-transform relative_l2_error
+ * (analysis.cpp:41-57, the same sequential sums, bit-identical) of the
+ * forward against the FP64 reference of the ingested input, or of
+ * inverse(forward(x)) against x; median over finite transforms, max (+inf if
+ * any non-finite) and the non-finite count (analysis.cpp:16-22,142-152).
+ * `errs` (optional, `batch` doubles, host) receives the per-transform errors.
+ * dsfft_error_device == dsfft_error_device_ex(..., DSFFT_REF_AUTO, ...). */
 int dsfft_error_device(dsfft_plan plan, int metric, const void* d_x, size_t batch, void* stream,
                        dsfft_error_report* out, double* errs);
+int dsfft_error_device_ex(dsfft_plan plan, int metric, int reference, const void* d_x,
+                          size_t batch, void* stream, dsfft_error_report* out, double* errs);
+
+/* dft_oracle (fft.hpp:44, fft.cpp:103-121) on the device, bit-identical:
+ * the reference's cos/sin per residue (j k) mod n, sequential k-order
+ * accumulation with separately rounded FP64 mul / add / sub.  Any n in
+ * [1, 2^24] (not only powers of two).  Interleaved (re, im) doubles.
+ *   dsfft_dft_device  device buffers (16-byte aligned, out of place), stream-ordered,
+ *                     returns after the kernel completes;
+ *   dsfft_dft_oracle  host buffers (the SampleBuffer carrier), synchronous. */
+int dsfft_dft_device(const void* d_in, void* d_out, size_t n, size_t batch, int device,
+                     void* stream);
+int dsfft_dft_oracle(const double* in, double* out, size_t n, size_t batch, int device);
 
 /* measure_error(n, strategy, precision, metric, trials, seed)
  * (analysis.cpp:101-154): the reference's protocol (one SplitMix64 stream,
- * re then im, ingest round_to) with every transform on `device`.  The FP64
- * reference is the device fp64 transform instead of the O(n^2) dft_oracle
- * (both FP64-accurate; errors agree to ~1e-9 relative). */
+ * re then im, ingest round_to) with every transform on `device`.  For
+ * n <= 2^16 the FP64 reference is the device dft_oracle and the report is
+ * bit-identical to the reference's; beyond, the fp64 FFT (O(n^2) DFTs of 2^20
+ * points take seconds each). */
 int dsfft_measure_error(size_t n, int strategy, int precision, int metric, size_t trials,
                         uint64_t seed, int device, dsfft_error_report* out);
+
+/* Synthetic batch on the device, keyed by the GLOBAL transform index: fills
+ * `count` transforms of n samples (working precision) with transforms
+ * [first_transform, first_transform + count) of the batch defined by `seed`.
+ * Component c of sample s of transform b is uniform [-1, 1) (the
+ * reference's 53-bit construction, analysis.hpp:84-87) from a splitmix64 hash
+ * of (seed, 2(b n + s) + c), rounded once into `precision`.  A shard generated
+ * on any device equals the same rows of the whole batch generated on one
+ * (the multi-GPU bench checks its shards this way).  Stream-ordered. */
+int dsfft_fill_uniform(void* d_out, size_t n, uint64_t first_transform, size_t count,
+                       uint64_t seed, int precision, int device, void* stream);
 
 /* round_to (precision.cpp:61-75) of `count` doubles into the working format
  * (binary16 / binary32 words), and the exact widening back. */

@@ -3,10 +3,15 @@
 // butterfly,fft}.hpp), header-only over the C ABI in dsfft.h.
 //
 // Same type names, fields, signatures, argument meaning and exceptions as the
-// reference, so a caller switches with
+// reference for everything on the plan/execute/analysis path, so a caller
+// switches with
 //     #include "fmafft_b200.hpp"
 //     namespace fmafft = fmafft_b200;
-// and links libdsfft.so.  Differences a caller can observe:
+// (or keeps its `#include "fmafft/fft.hpp"` lines and puts include/ first on
+// the include path: include/fmafft/*.hpp forward here) and links libdsfft.so.
+// The reference's own tests/test_fft.cpp, test_twiddle.cpp and acceptance
+// criteria 2-9 compile unmodified against this header (tests/test_cpp_compat.py).
+// Differences a caller can observe:
 //   * forward/inverse run on the plan's B200; fp32 and fp16 results are
 //     bit-identical to the reference (its ArithmeticContext rounding).
 //   * ArithmeticContext counters are advanced analytically by the exact
@@ -17,9 +22,21 @@
 //     reference's fp64 path).
 //   * Batched overloads (forward_batch / inverse_batch) transform many
 //     SampleBuffers in one call; device-buffer execution is dsfft_execute.
-//   * measure_error runs every trial on the device; its FP64 reference is the
-//     device fp64 transform rather than the O(n^2) dft_oracle (both FP64
-//     accurate; statistics agree to ~1e-9 relative).
+//   * dft_oracle and measure_error run on the device; both are bit-identical
+//     to the reference (same cos/sin, same sequential FP64 sums), so
+//     measure_error reports equal the reference's for n <= 2^16 (beyond, its
+//     FP64 reference is the fp64 FFT: an O(n^2) DFT of 2^20 points takes
+//     seconds).
+//   * A plan's table may be edited after make_plan, exactly as with the
+//     reference's plain-struct FftPlan: the next forward/inverse notices and
+//     runs with the edited records (dsfft_plan_create_with_table).
+//   * NOT provided (compile-time error with a message when used): the
+//     per-butterfly CPU kernels butterfly_standard / _linzer_feig / _cosine /
+//     _dual and kernel_for (butterfly.hpp:22-61), and the scalar emulator
+//     operations ArithmeticContext::add/sub/mul/fma (precision.hpp:38-62).
+//     They are the reference's CPU emulation; here butterflies exist only
+//     inside the device FFT, selected by the plan's Strategy, and there is no
+//     CPU arithmetic path.
 //   * The analysis / serialize surface the CLI uses (table_stats, the bound
 //     tables, write_table_csv, write_bounds_csv, write_error_csv) is mirrored
 //     with byte-identical CSV output.
@@ -30,6 +47,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <limits>
 #include <memory>
 #include <numbers>
 #include <ostream>
@@ -41,6 +59,13 @@
 #include "dsfft.h"
 
 namespace fmafft_b200 {
+
+namespace detail {
+// false, but only once instantiated: the static_assert of an unavailable
+// reference function fires where the caller uses it, not here
+template <class...>
+inline constexpr bool kUnavailable = false;
+}  // namespace detail
 
 // precision.hpp:12-62
 enum class Precision { fp16, fp32, fp64 };
@@ -71,6 +96,22 @@ class ArithmeticContext {
   Precision precision() const { return precision_; }
   const OpCounter& counters() const { return counters_; }
   void reset_counters() { counters_.reset(); }
+  // The reference's scalar emulator ops (precision.cpp:77-111) are its CPU
+  // arithmetic; this library has none -- every rounding happens inside the
+  // device FFT.  Using one is a compile-time error:
+  template <class... A>
+  double fma(A...) {
+    static_assert(detail::kUnavailable<A...>,
+                  "fmafft_b200: ArithmeticContext::fma/add/sub/mul (scalar CPU emulation) "
+                  "are not provided; transforms round on the device (forward/inverse)");
+    return 0.0;
+  }
+  template <class... A>
+  double add(A... a) { return fma(a...); }
+  template <class... A>
+  double sub(A... a) { return fma(a...); }
+  template <class... A>
+  double mul(A... a) { return fma(a...); }
   // analytic accounting used by forward/inverse below
   void account(std::uint64_t fma, std::uint64_t add, std::uint64_t mul) {
     counters_.fma_count += fma;
@@ -129,6 +170,29 @@ struct ButterflyResult {
   ComplexSample sum;
   ComplexSample diff;
 };
+
+// butterfly.hpp:22-61: the per-butterfly plugin point.  The type exists so
+// signatures compile; the CPU kernels do not.  On this library the plan's
+// Strategy selects the butterfly of the device FFT (csrc/fft_kernels.cuh),
+// where COS / SIN forms are chosen per twiddle by the table record.
+using ButterflyKernel = ButterflyResult (*)(const ComplexSample&, const ComplexSample&,
+                                            const TwiddleEntry&, ArithmeticContext&);
+#define FMAFFT_B200_NO_CPU_BUTTERFLY                                                            \
+  static_assert(detail::kUnavailable<A...>,                                                  \
+                "fmafft_b200: butterfly_* / kernel_for (butterfly.hpp:22-61) are the "         \
+                "reference's CPU kernels and are not provided; butterflies run only inside "   \
+                "the device FFT -- select the variant with make_plan(n, Strategy, Precision)")
+template <class... A>
+ButterflyResult butterfly_standard(A&&...) { FMAFFT_B200_NO_CPU_BUTTERFLY; return {}; }
+template <class... A>
+ButterflyResult butterfly_linzer_feig(A&&...) { FMAFFT_B200_NO_CPU_BUTTERFLY; return {}; }
+template <class... A>
+ButterflyResult butterfly_cosine(A&&...) { FMAFFT_B200_NO_CPU_BUTTERFLY; return {}; }
+template <class... A>
+ButterflyResult butterfly_dual(A&&...) { FMAFFT_B200_NO_CPU_BUTTERFLY; return {}; }
+template <class... A>
+ButterflyKernel kernel_for(A&&...) { FMAFFT_B200_NO_CPU_BUTTERFLY; return nullptr; }
+#undef FMAFFT_B200_NO_CPU_BUTTERFLY
 
 // fft.hpp:12-44
 using SampleBuffer = std::vector<ComplexSample>;
@@ -191,16 +255,66 @@ inline double round_to(double x, Precision p) {
   return out;
 }
 
-// Immutable execution recipe (fft.hpp:17-23) plus the device plan it owns.
+// Execution recipe (fft.hpp:17-23) plus the device plan it owns.  Like the
+// reference's plain struct, copies share nothing observable: editing
+// `table` of one copy affects only that copy's next forward/inverse.
 struct FftPlan {
   std::size_t n = 0;
   unsigned m = 0;
   Strategy strategy = Strategy::standard;
   Precision precision = Precision::fp64;
   TwiddleTable table;
-  std::shared_ptr<std::remove_pointer_t<dsfft_plan>> device;  // shared, immutable
-  dsfft_plan handle() const { return device.get(); }
+  int device_ordinal = 0;
+  // device plan and the exact table it was built from (shared by copies,
+  // replaced when this copy's table is edited)
+  mutable std::shared_ptr<std::remove_pointer_t<dsfft_plan>> device;
+  mutable std::shared_ptr<const TwiddleTable> uploaded;
+  dsfft_plan handle() const;
 };
+
+namespace detail {
+inline bool same_bits(double a, double b) {
+  return std::bit_cast<std::uint64_t>(a) == std::bit_cast<std::uint64_t>(b);
+}
+inline bool same_table(const TwiddleTable& a, const TwiddleTable& b) {
+  if (a.n != b.n || a.strategy != b.strategy || a.entries.size() != b.entries.size())
+    return false;
+  for (std::size_t k = 0; k < a.entries.size(); ++k) {
+    const TwiddleEntry &x = a.entries[k], &y = b.entries[k];
+    if (!same_bits(x.multiplier, y.multiplier) || !same_bits(x.ratio, y.ratio) ||
+        x.path != y.path || x.clamped != y.clamped || !same_bits(x.omega_r, y.omega_r) ||
+        !same_bits(x.omega_i, y.omega_i))
+      return false;
+  }
+  return true;
+}
+inline std::vector<dsfft_entry> raw_entries(const TwiddleTable& t) {
+  std::vector<dsfft_entry> raw(t.entries.size());
+  for (std::size_t k = 0; k < raw.size(); ++k) {
+    const TwiddleEntry& e = t.entries[k];
+    raw[k] = dsfft_entry{e.multiplier, e.ratio, e.path == TwiddlePath::sin ? 1 : 0,
+                         e.clamped ? 1 : 0, e.omega_r, e.omega_i};
+  }
+  return raw;
+}
+}  // namespace detail
+
+// The device plan for the plan's CURRENT fields and table (rebuilt from the
+// edited records when they no longer match what was uploaded).
+inline dsfft_plan FftPlan::handle() const {
+  if (device && uploaded && uploaded->n == n && detail::same_table(*uploaded, table) &&
+      table.strategy == strategy)
+    return device.get();
+  if (table.entries.size() != n / 2)
+    throw std::invalid_argument("plan table does not hold n/2 entries");
+  const std::vector<dsfft_entry> raw = detail::raw_entries(table);
+  dsfft_plan h = nullptr;
+  detail::check(dsfft_plan_create_with_table(n, int(strategy), int(precision), raw.data(),
+                                             raw.size(), device_ordinal, &h));
+  device.reset(h, detail::PlanDeleter{});
+  uploaded = std::make_shared<const TwiddleTable>(table);
+  return h;
+}
 
 // fft.cpp:56-72: n a power of two in [2, 2^24]; the table is built in FP64
 // and every scalar rounded once into the working precision.
@@ -210,6 +324,7 @@ inline FftPlan make_plan(std::size_t n, Strategy strategy, Precision precision,
   detail::check(dsfft_plan_create(n, int(strategy), int(precision), 1e-7, device, &h));
   FftPlan p;
   p.device.reset(h, detail::PlanDeleter{});
+  p.device_ordinal = device;
   unsigned m = 0;
   detail::check(dsfft_plan_info(h, &p.n, &m, nullptr, nullptr));
   p.m = m;
@@ -219,6 +334,7 @@ inline FftPlan make_plan(std::size_t n, Strategy strategy, Precision precision,
   detail::check(dsfft_plan_table(h, raw.data(), raw.size()));
   raw.resize(n / 2);
   p.table = detail::to_table(n, strategy, raw);
+  p.uploaded = std::make_shared<const TwiddleTable>(p.table);
   return p;
 }
 
@@ -279,6 +395,19 @@ inline std::vector<SampleBuffer> inverse_batch(const FftPlan& plan,
                                                const std::vector<SampleBuffer>& spectra,
                                                ArithmeticContext& ctx) {
   return detail::run(plan, spectra, ctx, DSFFT_INVERSE);
+}
+
+// fft.hpp:44, fft.cpp:103-121: the O(n^2) FP64 DFT, on the device and
+// bit-identical to the reference (same cos/sin per residue (j k) mod n, the
+// same sequential k-order sums with separately rounded operations).  Any n.
+inline SampleBuffer dft_oracle(const SampleBuffer& input, int device = 0) {
+  const std::size_t n = input.size();
+  SampleBuffer out(n);
+  if (n == 0) return out;
+  static_assert(sizeof(ComplexSample) == 2 * sizeof(double), "SampleBuffer carrier layout");
+  detail::check(dsfft_dft_oracle(reinterpret_cast<const double*>(input.data()),
+                                 reinterpret_cast<double*>(out.data()), n, 1, device));
+  return out;
 }
 
 // ---- twiddle.hpp: angles and ratio statistics --------------------------------
@@ -366,6 +495,43 @@ inline std::vector<BoundReport> reproduce_cumulative_table(std::size_t n,
   rows[1].improvement_vs_baseline = rows[0].cumulative_bound / rows[1].cumulative_bound;
   return rows;
 }
+
+// analysis.cpp:41-57 (host: an O(n) reduction of two SampleBuffers the caller
+// already holds; the reference's sequential sums, so identical results when
+// compiled without FP contraction -- the default on x86-64)
+inline double relative_l2_error(const SampleBuffer& x, const SampleBuffer& y) {
+  if (x.size() != y.size()) throw std::invalid_argument("relative_l2_error: length mismatch");
+  double num = 0.0, den = 0.0;
+  bool finite = true;
+  for (std::size_t i = 0; i < x.size(); ++i) {
+    if (!std::isfinite(x[i].re) || !std::isfinite(x[i].im)) finite = false;
+    const double dr = x[i].re - y[i].re;
+    const double di = x[i].im - y[i].im;
+    num += dr * dr + di * di;
+    den += y[i].re * y[i].re + y[i].im * y[i].im;
+  }
+  if (den == 0.0) throw std::invalid_argument("relative_l2_error: all-zero reference");
+  if (!finite) return std::numeric_limits<double>::infinity();
+  return std::sqrt(num / den);
+}
+
+// analysis.hpp:70-91: the deterministic generator of the reference's input
+// protocol (golden-gamma increment, splitmix64 finalizer).
+class SplitMix64 {
+ public:
+  explicit SplitMix64(std::uint64_t seed) : state_(seed) {}
+  std::uint64_t next() {
+    std::uint64_t z = (state_ += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  // uniform in [-1, 1): top 53 bits scaled to [0, 1), then 2u - 1 (exact)
+  double uniform_pm1() { return 2.0 * (static_cast<double>(next() >> 11) * 0x1p-53) - 1.0; }
+
+ private:
+  std::uint64_t state_;
+};
 
 enum class ErrorMetric { roundtrip, forward_vs_oracle };
 inline std::string_view to_string(ErrorMetric m) {

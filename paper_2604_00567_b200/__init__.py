@@ -24,8 +24,9 @@ import numpy as np
 __all__ = ["Strategy", "Precision", "FftPlan", "make_plan", "forward", "inverse",
            "execute", "forward_f64", "inverse_f64", "execute_host", "execute_multi",
            "round_to", "widen", "build_table", "table_csv", "bounds_csv", "error_device",
-           "measure_error", "last_launch_count", "parse_strategy", "parse_precision",
-           "library_path", "DsfftError"]
+           "measure_error", "dft_oracle", "dft_device", "make_plan_from_table", "fill_uniform", "synthetic_batch",
+           "last_launch_count", "parse_strategy", "parse_precision", "library_path",
+           "DsfftError"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # DSFFT_LIBRARY: load another build of the library (A/B timing of two builds)
@@ -166,6 +167,23 @@ def make_plan(n: int, strategy: str = "dual", precision: str = "fp32",
     return FftPlan(int(n), m, strategy, precision, device, h)
 
 
+def make_plan_from_table(n: int, strategy: str, precision: str, table: np.ndarray,
+                         device: int = 0) -> FftPlan:
+    """A plan over a caller-supplied rounded table (FftPlan::table.entries,
+    possibly edited -- the reference's FftPlan is a plain struct): the records
+    are packed and uploaded as given (dsfft_plan_create_with_table)."""
+    strategy = parse_strategy(strategy)
+    precision = parse_precision(precision)
+    t = np.ascontiguousarray(table, dtype=ENTRY_DTYPE)
+    lib = _load()
+    lib.dsfft_plan_create_with_table.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_void_p,
+                                                 C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]
+    h = C.c_void_p()
+    _check(lib.dsfft_plan_create_with_table(int(n), STRATEGIES[strategy], PRECISIONS[precision],
+                                            t.ctypes.data, t.size, int(device), C.byref(h)))
+    return FftPlan(int(n), int(n).bit_length() - 1, strategy, precision, device, h)
+
+
 def bounds_csv(n: int, kind: str = "stats", precision: str = "fp16") -> str:
     """write_bounds_csv (serialize.cpp:79-91) of reproduce_ratio_table(n)
     (kind "stats": the CLI `stats` command) or reproduce_cumulative_table(n,
@@ -235,8 +253,21 @@ def _torch_view(x, plan: FftPlan):
         raise ValueError("device API needs a CUDA tensor (use forward_f64 for host data)")
     if not x.is_contiguous():
         raise ValueError("tensor must be contiguous")
+    if x.device.index != plan.device:
+        raise ValueError(f"tensor is on cuda:{x.device.index}, plan on cuda:{plan.device}")
     batch = x.numel() // (plan.n * (2 if x.dtype == want_r else 1))
     return batch
+
+
+def _check_out(x, out) -> None:
+    """`out` must be a buffer the kernels can write exactly like `x`."""
+    if out.dtype != x.dtype or out.numel() != x.numel():
+        raise ValueError(f"out ({out.dtype}, {out.numel()} elements) does not match the input "
+                         f"({x.dtype}, {x.numel()} elements)")
+    if not out.is_cuda or out.device.index != x.device.index:
+        raise ValueError("out must be on the same CUDA device as the input")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
 
 
 def execute(plan: FftPlan, direction: int, x, out=None, stream=None):
@@ -245,6 +276,8 @@ def execute(plan: FftPlan, direction: int, x, out=None, stream=None):
     batch = _torch_view(x, plan)
     if out is None:
         out = torch.empty_like(x)
+    else:
+        _check_out(x, out)
     if stream is None:
         stream = torch.cuda.current_stream(x.device).cuda_stream
     _check(_load().dsfft_execute(plan._handle, direction, x.data_ptr(), out.data_ptr(), batch,
@@ -349,24 +382,100 @@ def _report(rep: "_ErrorReport") -> dict:
 
 
 _METRICS = {"roundtrip": 0, "forward": 1, "forward_vs_oracle": 1}
+_REFERENCES = {"auto": 0, "dft": 1, "fft64": 2}
 
 
 def error_device(plan: FftPlan, x, metric: str = "forward", stream=None,
-                 per_transform: bool = False):
-    """Device error harness over a device batch (dsfft_error_device): the
-    reference's ErrorReport (analysis.hpp:58-68) for every transform in `x`."""
+                 per_transform: bool = False, reference: str = "auto"):
+    """Device error harness over a device batch (dsfft_error_device_ex): the
+    reference's ErrorReport (analysis.hpp:58-68) for every transform in `x`.
+    reference: "dft" (dft_oracle, bit-identical reports), "fft64" (the fp64
+    FFT) or "auto" (DFT for n <= 4096)."""
     import torch
     batch = _torch_view(x, plan)
+    if reference not in _REFERENCES:
+        raise ValueError(f"unknown error reference: {reference}")
     lib = _load()
-    lib.dsfft_error_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p,
-                                       C.POINTER(_ErrorReport), C.c_void_p]
+    lib.dsfft_error_device_ex.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                                          C.c_void_p, C.POINTER(_ErrorReport), C.c_void_p]
     rep = _ErrorReport()
     errs = np.empty(batch, dtype=np.float64) if per_transform else None
     if stream is None:
         stream = torch.cuda.current_stream(x.device).cuda_stream
-    _check(lib.dsfft_error_device(plan._handle, _METRICS[metric], x.data_ptr(), batch, stream,
-                                  C.byref(rep), errs.ctypes.data if errs is not None else None))
+    _check(lib.dsfft_error_device_ex(plan._handle, _METRICS[metric], _REFERENCES[reference],
+                                     x.data_ptr(), batch, stream, C.byref(rep),
+                                     errs.ctypes.data if errs is not None else None))
     return (_report(rep), errs) if per_transform else _report(rep)
+
+
+def fill_uniform(out, n: int, first_transform: int, seed: int, precision: str,
+                 stream=None):
+    """dsfft_fill_uniform: fill the CUDA tensor `out` (working precision,
+    [count, n, 2] or complex) with transforms [first, first + count) of the
+    synthetic batch `seed` -- keyed by the global transform index, so a shard
+    equals the same rows of the whole batch."""
+    import torch
+    p = PRECISIONS[parse_precision(precision)]
+    want = {0: torch.float16, 1: torch.float32, 2: torch.float64}[p]
+    if out.dtype not in (want, {0: torch.complex32, 1: torch.complex64,
+                                2: torch.complex128}[p]):
+        raise ValueError(f"{precision} batch needs {want} storage, got {out.dtype}")
+    if not out.is_cuda or not out.is_contiguous():
+        raise ValueError("fill_uniform needs a contiguous CUDA tensor")
+    comps = out.numel() * (2 if out.is_complex() else 1)
+    if comps % (2 * n):
+        raise ValueError("tensor does not hold whole transforms of n samples")
+    if stream is None:
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    lib = _load()
+    lib.dsfft_fill_uniform.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_size_t,
+                                       C.c_uint64, C.c_int, C.c_int, C.c_void_p]
+    _check(lib.dsfft_fill_uniform(out.data_ptr(), int(n), int(first_transform),
+                                  comps // (2 * n), int(seed), p, out.device.index, stream))
+    return out
+
+
+def synthetic_batch(n: int, first_transform: int, count: int, seed: int, precision: str,
+                    device: int = 0, stream=None):
+    """A new [count, n, 2] CUDA tensor from fill_uniform."""
+    import torch
+    dt = {"fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[
+        parse_precision(precision)]
+    out = torch.empty((count, n, 2), dtype=dt, device=torch.device("cuda", device))
+    return fill_uniform(out, n, first_transform, seed, precision, stream)
+
+
+def dft_oracle(x, device: int = 0) -> np.ndarray:
+    """fmafft::dft_oracle (fft.hpp:44, fft.cpp:103-121) on the device,
+    bit-identical: complex128 [..., n] in and out (any n)."""
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    n = x.shape[-1]
+    out = np.empty_like(x)
+    lib = _load()
+    lib.dsfft_dft_oracle.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int]
+    _check(lib.dsfft_dft_oracle(x.ctypes.data, out.ctypes.data, n, x.size // max(n, 1),
+                                int(device)))
+    return out
+
+
+def dft_device(x, out=None, stream=None):
+    """dft_oracle over a CUDA complex128 tensor [..., n] (stream-ordered)."""
+    import torch
+    if x.dtype != torch.complex128 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("dft_device needs a contiguous CUDA complex128 tensor")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _check_out(x, out)
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    n = x.shape[-1]
+    lib = _load()
+    lib.dsfft_dft_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int,
+                                     C.c_void_p]
+    _check(lib.dsfft_dft_device(x.data_ptr(), out.data_ptr(), n, x.numel() // max(n, 1),
+                                x.device.index, stream))
+    return out
 
 
 def measure_error(n: int, strategy: str, precision: str, metric: str = "forward",

@@ -113,12 +113,14 @@ void fp64_destroy(F64Plan* fp) { delete fp; }
 int fp64_execute(F64Plan& fp, bool inverse, const void* in, void* out, size_t batch,
                  double scale, int sm_count, cudaStream_t st, uint64_t* launches) {
   const int m = fp.m;
-  const size_t bytes = (size_t(1) << m) * sizeof(double2) * batch;
-  // per-call, stream-ordered ping-pong buffers (plans may run on several streams)
+  const size_t tb = (size_t(1) << m) * sizeof(double2);
+  // per-call, stream-ordered ping-pong buffers (plans may run on several
+  // streams), at most 256 MiB each: the batch runs in chunks
+  const size_t chunk = std::max<size_t>(1, std::min(batch, (size_t(256) << 20) / tb));
   double2* scratch[2] = {nullptr, nullptr};
   if (m > 1)
     for (auto*& sp : scratch)
-      if (scratch_alloc(reinterpret_cast<void**>(&sp), bytes, st) != cudaSuccess) {
+      if (scratch_alloc(reinterpret_cast<void**>(&sp), chunk * tb, st) != cudaSuccess) {
         scratch_free(scratch[0], st);
         g_f64_err = "fp64: scratch allocation failed";
         return 1;
@@ -131,31 +133,36 @@ int fp64_execute(F64Plan& fp, bool inverse, const void* in, void* out, size_t ba
       scratch_free(s[1], st);
     }
   } release{scratch, st};
-  const long long total = (long long)batch << (m - 1);
-  const int grid = int(std::min<long long>((total + 255) / 256, (long long)sm_count * 8));
   const bool std_ = fp.strategy == kStandard;
-  for (int p = 0; p < m; ++p) {
-    const double2* X = p == 0 ? static_cast<const double2*>(in) : scratch[(p - 1) & 1];
-    double2* Y = p == m - 1 ? static_cast<double2*>(out) : scratch[p & 1];
-    const bool ci = inverse && p == 0, so = inverse && p == m - 1;
-    auto go = [&](auto kern) { kern<<<grid, 256, 0, st>>>(X, Y, fp.d_tab, total, m, p, scale); };
-    if (std_) {
-      if (ci && so) go(fft64_pass<true, true, true>);
-      else if (ci) go(fft64_pass<true, true, false>);
-      else if (so) go(fft64_pass<true, false, true>);
-      else go(fft64_pass<true, false, false>);
-    } else {
-      if (ci && so) go(fft64_pass<false, true, true>);
-      else if (ci) go(fft64_pass<false, true, false>);
-      else if (so) go(fft64_pass<false, false, true>);
-      else go(fft64_pass<false, false, false>);
+  for (size_t b0 = 0; b0 < batch; b0 += chunk) {
+    const size_t nb = std::min(chunk, batch - b0);
+    const long long total = (long long)nb << (m - 1);
+    const int grid = int(std::min<long long>((total + 255) / 256, (long long)sm_count * 8));
+    const double2* src = static_cast<const double2*>(in) + (b0 << m);
+    double2* dst = static_cast<double2*>(out) + (b0 << m);
+    for (int p = 0; p < m; ++p) {
+      const double2* X = p == 0 ? src : scratch[(p - 1) & 1];
+      double2* Y = p == m - 1 ? dst : scratch[p & 1];
+      const bool ci = inverse && p == 0, so = inverse && p == m - 1;
+      auto go = [&](auto kern) { kern<<<grid, 256, 0, st>>>(X, Y, fp.d_tab, total, m, p, scale); };
+      if (std_) {
+        if (ci && so) go(fft64_pass<true, true, true>);
+        else if (ci) go(fft64_pass<true, true, false>);
+        else if (so) go(fft64_pass<true, false, true>);
+        else go(fft64_pass<true, false, false>);
+      } else {
+        if (ci && so) go(fft64_pass<false, true, true>);
+        else if (ci) go(fft64_pass<false, true, false>);
+        else if (so) go(fft64_pass<false, false, true>);
+        else go(fft64_pass<false, false, false>);
+      }
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        g_f64_err = std::string("fft64_pass launch: ") + cudaGetErrorString(e);
+        return 1;
+      }
+      if (launches) ++*launches;
     }
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-      g_f64_err = std::string("fft64_pass launch: ") + cudaGetErrorString(e);
-      return 1;
-    }
-    if (launches) ++*launches;
   }
   return 0;
 }

@@ -32,6 +32,19 @@ uint32_t f32_bits(double x) {
 
 }  // namespace
 
+std::vector<double> dft_table(std::size_t n) {
+  // dft_oracle (fft.cpp:103-121): theta = -two_pi_over_n * ((j k) mod n) with
+  // two_pi_over_n = (2 pi) / n, then libm cos / sin -- tabulated per residue
+  std::vector<double> t(2 * n);
+  const double two_pi_over_n = (2.0 * kPi) / static_cast<double>(n);
+  for (std::size_t r = 0; r < n; ++r) {
+    const double theta = -two_pi_over_n * static_cast<double>(r);
+    t[2 * r] = std::cos(theta);
+    t[2 * r + 1] = std::sin(theta);
+  }
+  return t;
+}
+
 double twiddle_angle(std::size_t k, std::size_t n) {
   return -(2.0 * kPi) * (static_cast<double>(k) / static_cast<double>(n));
 }

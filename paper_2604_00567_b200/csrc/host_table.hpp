@@ -37,6 +37,10 @@ struct InvalidArgument : std::invalid_argument {
 // theta_k = -(2 pi) * (k / n)
 double twiddle_angle(std::size_t k, std::size_t n);
 
+// dft_oracle's twiddles (fft.cpp:103-121), indexed by r = (j k) mod n:
+// interleaved (cos theta_r, sin theta_r), 2n doubles, any n >= 1.
+std::vector<double> dft_table(std::size_t n);
+
 // FP64 table of n/2 entries (throws InvalidArgument like the reference).
 std::vector<TableEntry> build_table(std::size_t n, int strategy, double clamp_eps);
 

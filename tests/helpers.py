@@ -46,3 +46,17 @@ def max_ulp_fp16(a: np.ndarray, b: np.ndarray) -> int:
     if not fin.any():
         return 0
     return int(np.max(np.abs(ordered(a[fin]) - ordered(b[fin]))))
+
+
+def synth_reference(n: int, first: int, count: int, seed: int) -> np.ndarray:
+    """NumPy restatement of dsfft_fill_uniform (csrc/synth.cu) before the
+    working-precision rounding: float64 [count, n, 2] uniform [-1, 1) from a
+    splitmix64 hash of (seed, global component index)."""
+    with np.errstate(over="ignore"):
+        c = np.uint64(2 * first * n) + np.arange(2 * n * count, dtype=np.uint64)
+        z = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * (c + np.uint64(1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return (2.0 * u - 1.0).reshape(count, n, 2)

@@ -22,7 +22,8 @@ def test_reference_arm_json_line(orc, ref):
         assert key in d, key
     assert d["impl"] == "reference"
     assert d["metric"] == "batched FFT transforms/s" and d["unit"] == "transforms/s"
-    assert d["value"] > 0 and d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["scaling"] == "strong"
+    assert d["config"]["global_batch"] == 1 << 20 and d["cpu_baseline"]["cpu_model"]
     assert d["steps"] == 1 and d["warmup"] == 0 and d["n_gpus"] == 1
     assert d["dtype"] == "f16" and d["vs_baseline"] is None
     assert "workload" in d["config"] and d["config"]["n"] == 1024

@@ -366,8 +366,12 @@ def test_plan_lifecycle_releases_device_memory(dsfft, cuda):
         gc.collect()
         cuda.cuda.synchronize()
 
-    cycle()  # first use: module loads, pools, cuBLAS-free context setup
+    cuda.cuda.synchronize()
+    before, _ = cuda.cuda.mem_get_info()
+    cycle()  # first use: lazy module loads (kernel code), context setup
     free0, _ = cuda.cuda.mem_get_info()
+    # scratch pools are trimmed on plan destroy: only kernel code stays
+    assert before - free0 < (128 << 20), (before, free0)
     for _ in range(5):
         cycle()
     free1, _ = cuda.cuda.mem_get_info()
