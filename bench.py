@@ -278,7 +278,7 @@ def self_launch(args) -> int:
     """--gpus N outside torchrun: run this script under torch.distributed.run."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
-           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+           f"--master-port={_free_port()}", "--", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.run(cmd).returncode
 
 

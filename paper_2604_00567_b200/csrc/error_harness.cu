@@ -108,10 +108,11 @@ __global__ void __launch_bounds__(256) dft_kernel(const double2* __restrict__ x,
     }
     for (int j0 = threadIdx.x; j0 < n; j0 += blockDim.x * JT) {
       double ar[JT], ai[JT];
-      int jj[JT], r[JT];
+      int jj[JT], js[JT], r[JT];
 #pragma unroll
       for (int t = 0; t < JT; ++t) {
         jj[t] = j0 + t * int(blockDim.x);
+        js[t] = jj[t] < n ? jj[t] : 0;  // outputs past n: keep r in range, never stored
         ar[t] = 0.0;
         ai[t] = 0.0;
         r[t] = 0;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) dft_kernel(const double2* __restrict__ x,
           // acc_re += re*c - im*s; acc_im += re*s + im*c, each op rounded
           ar[t] = __dadd_rn(ar[t], __dsub_rn(__dmul_rn(v.x, w.x), __dmul_rn(v.y, w.y)));
           ai[t] = __dadd_rn(ai[t], __dadd_rn(__dmul_rn(v.x, w.y), __dmul_rn(v.y, w.x)));
-          r[t] += jj[t];
+          r[t] += js[t];
           if (r[t] >= n) r[t] -= n;
         }
       }
