@@ -33,8 +33,7 @@
 #include <string>
 #include <vector>
 
-#include "fft_kernels.cuh"
-#include "multipass.cuh"
+#include "multipass_impl.cuh"
 #include "stream_alloc.cuh"
 
 namespace dsfft {
@@ -44,6 +43,7 @@ thread_local std::string g_mp_err;
 }
 
 const char* multipass_error() { return g_mp_err.c_str(); }
+void set_mp_error(const std::string& msg) { g_mp_err = msg; }
 
 struct MpParams {
   uint8_t* out;      // output of this pass group (chunk base)
@@ -54,40 +54,6 @@ struct MpParams {
   long long b_off;   // first transform of the chunk (tensor-map coordinate)
   long long tiles;   // nb * tiles_per_transform
   uint32_t scale;
-};
-
-// ---- twiddle table layouts (host and device agree) ---------------------------
-// first group (P = 0, twiddles independent of the column):
-//   [0, 31)                      stage 1, slot1 = 2^pl - 1 + rl
-//   31 + slot2*32 + r_l          stage 2, slot2 = 2^pl - 1 + rl, r_l < 32
-// later groups, per block of 32 columns (rb = r / 32), base rb * mp_block:
-//   slot1*32 + lane                          stage 1
-//   31*32 + (slot2*32 + r_l)*32 + lane       stage 2
-__host__ __device__ constexpr int mp_first_records(int S1) { return 31 + (((1 << S1) - 1) << 5); }
-__host__ __device__ constexpr int mp_block_records(int S1) {
-  return 31 * 32 + (((1 << S1) - 1) << 10);
-}
-
-template <int S1, class A>
-struct MpLayout {
-  static constexpr int s = 5 + S1, L = 1 << s, T = 32 << S1;
-  static constexpr int VB = A::kWords * 4;
-  static constexpr int kBufBytes = 32 * (L + 1) * VB;  // padded exchange >= TMA tile
-  static constexpr int kTileBytes = 32 * L * VB;
-  // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned
-  // later groups keep their column block's whole twiddle slab in smem (stage 1
-  // and 2) when it fits next to the ring (S1 <= 3: <= 65 KB with 8-byte fp16 pair
-  // records, 130 KB with 16-byte records); S1 = 4 stages
-  // only the stage-1 part and reads stage 2 through L1
-  static constexpr bool kFullSlab = S1 <= 3;
-  static constexpr int kSlabRecords = kFullSlab ? mp_block_records(S1) : 31 * 32;
-  __host__ __device__ static constexpr int tw_bytes(bool first) {
-    return ((first ? mp_first_records(S1) : kSlabRecords) * A::kRecBytes + 127) & ~127;
-  }
-  static size_t smem_bytes(bool first, int stages, int groups) {
-    const int tw = tw_bytes(first);
-    return size_t(tw) + size_t(groups) * stages * (kBufBytes + 8);
-  }
 };
 
 // One pass group over all tiles of a chunk.  A CTA runs G = blockDim/T tile
@@ -102,8 +68,7 @@ template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_O
 __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     mp_kernel(const __grid_constant__ CUtensorMap in_map, const MpParams p) {
   using Lay = MpLayout<S1, A>;
-  constexpr int L = Lay::L, T = Lay::T, NG2 = 32 >> S1, VB = Lay::VB;
-  constexpr int STRIDE = L + 1;  // padded exchange column (values)
+  constexpr int L = Lay::L, T = Lay::T;
   constexpr int ROWS_BOX = L < 256 ? L : 256;
   extern __shared__ __align__(128) uint8_t smem[];
   const int G = blockDim.x / T;
@@ -121,9 +86,6 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
                    g * S;
   const long long rblocks = FIRST ? 1 : ((1LL << P) >> 5);
   const bool leader = t == 0;
-  auto group_sync = [&]() {
-    if (T == 32) __syncwarp(); else ptx::named_bar_sync(1 + g, T);
-  };
 
   if constexpr (FIRST) {  // column-independent twiddles: stage once per CTA
     for (int i = threadIdx.x; i < (mp_first_records(S1) * RB + 15) / 16; i += blockDim.x)
@@ -145,8 +107,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   constexpr int HALF = 32 * L * EB;             // one transform's tile
   // fp16 pairs keep intermediates pair-packed: 8-byte values (re0,re1),(im0,im1)
   // of transforms (b, b+1) at pair index b/2 -- no unpack/repack between groups
-  constexpr bool PIN = PAIR == 2 && !FIRST, POUT = PAIR == 2 && !LAST;
-  constexpr int OEB = POUT ? 8 : EB;            // bytes per stored output element
+  constexpr bool PIN = PAIR == 2 && !FIRST;
   auto issue_load = [&](long long q, int rb, int b, int slot) {
     uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
     ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
@@ -164,176 +125,11 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
           ptx::tma_load_4d(d, &in_map, rb * 32, int(q), r0, bb, &bars[slot], pol);
       }
   };
-
-  // One tile: column block (q, rb) of transform b (and b+1 for pairs) from
-  // ring buffer `buf`; release() hands the slot back to TMA after its last read.
   auto tile = [&](long long q, int rb, int b, bool second, uint32_t buf, auto&& release) {
-    uint32_t re[32], im[32];
-    // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) --
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      [[maybe_unused]] const uint32_t a = buf + (((warp + (c << S1)) << 5) + lane) * VB;
-      if constexpr (PAIR == 2 && !PIN) {  // (re0,re1), (im0,im1) from the two halves
-        const uint32_t e = buf + (((warp + (c << S1)) << 5) + lane) * EB;
-        const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
-        re[c] = __byte_perm(lo, hi, 0x5410);
-        im[c] = __byte_perm(lo, hi, 0x7632);
-        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);  // conj on load (fft.cpp:90-91)
-      } else if constexpr (A::kWords == 1) {
-        re[c] = ptx::lds32(a);
-        if constexpr (CONJ_IN) re[c] ^= 0x80000000u;  // conj on load (fft.cpp:90-91)
-      } else {
-        ptx::lds64(a, re[c], im[c]);
-        if constexpr (CONJ_IN) im[c] = A::neg(im[c]);
-      }
-    }
-#pragma unroll
-    for (int pl = 0; pl < 5; ++pl) {
-      uint32_t nre[32], nim[32];
-#pragma unroll
-      for (int rl = 0; rl < (1 << pl); ++rl) {
-        const int slot1 = (1 << pl) - 1 + rl;
-        const uint4 tw = FIRST ? load_rec<A>(tw_base + slot1 * RB)
-                               : load_rec<A>(tw_base + (slot1 * 32 + lane) * RB);
-#pragma unroll
-        for (int qq = 0; qq < (16 >> pl); ++qq) {
-          const int jl = (qq << pl) | rl;
-          const int oa = (qq << (pl + 1)) + rl;
-          butterfly<A, STANDARD>(re[jl], im[jl], re[jl + 16], im[jl + 16], tw, nre[oa],
-                                 nim[oa], nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-        }
-      }
-#pragma unroll
-      for (int x = 0; x < 32; ++x) {
-        re[x] = nre[x];
-        if constexpr (A::kWords == 2) im[x] = nim[x];
-      }
-    }
-    // ---- exchange through the padded slot: [col][local pos] ---------------
-    group_sync();  // every stage-1 read of the TMA tile is done
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const uint32_t a = buf + (lane * STRIDE + warp * 32 + c) * VB;
-      if constexpr (A::kWords == 1) ptx::sts32(a, re[c]); else ptx::sts64(a, re[c], im[c]);
-    }
-    group_sync();
-    // stage 2 groups (column, r_l): first group lanes walk r_l (contiguous
-    // column output), later groups lanes walk columns (contiguous rows)
-#pragma unroll
-    for (int j = 0; j < NG2; ++j) {
-      const int col = FIRST ? warp + (j << S1) : lane;
-      const int rl_ = FIRST ? lane : warp + (j << S1);
-#pragma unroll
-      for (int c = 0; c < (1 << S1); ++c) {
-        const uint32_t a = buf + (col * STRIDE + rl_ + 32 * c) * VB;
-        const int v = (j << S1) + c;
-        if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
-      }
-    }
-    // release the slot to this group's tile S ahead
-    ptx::fence_proxy_async_smem();
-    group_sync();
-    release();
-    // ---- stage 2 ----------------------------------------------------------
-    [[maybe_unused]] const uint8_t* tw2 =
-        FIRST ? nullptr
-              : reinterpret_cast<const uint8_t*>(p.tw) +
-                    ((long long)rb * mp_block_records(S1) + 31 * 32 + warp * 32 + lane) * RB;
-#pragma unroll
-    for (int pl = 0; pl < S1; ++pl) {
-      uint32_t nre[32], nim[32];
-#pragma unroll
-      for (int rl = 0; rl < (1 << pl); ++rl)
-#pragma unroll
-        for (int j = 0; j < NG2; ++j) {
-          const int slot2 = (1 << pl) - 1 + rl;
-          uint4 tw;
-          if constexpr (FIRST)
-            tw = load_rec<A>(tw_base + (31 + (slot2 << 5) + lane) * RB);
-          else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
-            tw = load_rec<A>(tw_base + (31 * 32 + (warp << 5) + lane +
-                                        (((slot2 << 5) + (j << S1)) << 5)) * RB);
-          else  // r_l = warp + 2^S1 j
-            tw = ldg_rec<A>(tw2 + ((slot2 << 5) + (j << S1)) * 32 * RB);
-#pragma unroll
-          for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
-            const int jl = (qq << pl) | rl;
-            const int ia = (j << S1) + jl, ib = ia + (1 << (S1 - 1));
-            const int oa = (j << S1) + (qq << (pl + 1)) + rl;
-            butterfly<A, STANDARD>(re[ia], im[ia], re[ib], im[ib], tw, nre[oa], nim[oa],
-                                   nre[oa + (1 << pl)], nim[oa + (1 << pl)]);
-          }
-        }
-#pragma unroll
-      for (int x = 0; x < 32; ++x) {
-        re[x] = nre[x];
-        if constexpr (A::kWords == 2) im[x] = nim[x];
-      }
-    }
-    // ---- scatter ------------------------------------------------------------
-    // Stockham order: q*2^(P+s) + r + 2^P*(r_l + 32 c').  BOUT (the group
-    // feeding the last one) writes the blocked intermediate instead:
-    //   Z[(r' >> 5) * 2^s3 + c][r' & 31],  r' = r + 2^P c', c = q,
-    // so each last-group tile (32 columns r' x 2^s3 rows c) is one contiguous
-    // block.  Element offsets in units of one stored complex (EB bytes).
-    uint8_t* gout = p.out + b * N * EB;  // == pair b/2 * N * 8 for packed pairs
-    [[maybe_unused]] const long long S3 = N >> (P + Lay::s);  // rows of the last group (BOUT)
-    uint8_t* base;
-    long long jstride, cstride;  // bytes between values j<<S1 and rows c'
-    if constexpr (FIRST && BOUT) {  // r' = lane + 32 c, c-index = column
-      base = gout + ((q * 32 + warp) * 32 + lane) * OEB;
-      jstride = 32LL * OEB;
-      cstride = S3 * 32 * OEB;
-    } else if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
-      base = gout + ((q * 32 + warp) * L + lane) * OEB;
-      jstride = (long long)L * OEB;
-      cstride = 32 * OEB;
-    } else if constexpr (BOUT) {  // r' = rb*32 + lane + 2^P (warp + 2^S1 j + 32 c)
-      base = gout + (((rb + ((long long)warp << (P - 5))) * S3 + q) * 32 + lane) * OEB;
-      jstride = (S3 * 32 * OEB) << (P - 5);
-      cstride = ((S3 * 32 * OEB) << (P - 5)) * 32;
-    } else {
-      base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * OEB;
-      jstride = (long long)OEB << P;
-      cstride = ((long long)OEB << P) * 32;
-    }
-#pragma unroll
-    for (int j = 0; j < NG2; ++j)
-#pragma unroll
-      for (int c = 0; c < (1 << S1); ++c) {
-        const int v = (j << S1) + c;
-        uint32_t xr = re[v];
-        [[maybe_unused]] uint32_t xi = im[v];
-        if constexpr (SCALE_OUT) {  // conj + 1/n, one rounded mul each (fft.cpp:94-98)
-          if constexpr (A::kWords == 1) {
-            xr = A::mul(xr ^ 0x80000000u, p.scale);
-          } else {
-            xr = A::mul(xr, p.scale);
-            xi = A::mul(A::neg(xi), p.scale);
-          }
-        }
-        uint8_t* dst = base + (j << S1) * jstride + c * cstride;
-        if constexpr (POUT) {  // pair-packed intermediate
-          __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
-        } else if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
-          unsigned int* d0 = reinterpret_cast<unsigned int*>(dst);
-          unsigned int* d1 = reinterpret_cast<unsigned int*>(dst + N * EB);
-          const uint32_t t0 = __byte_perm(xr, xi, 0x5410), t1 = __byte_perm(xr, xi, 0x7632);
-          if constexpr (LAST) {
-            __stcs(d0, t0);
-            if (second) __stcs(d1, t1);
-          } else {
-            __stcg(d0, t0);
-            if (second) __stcg(d1, t1);
-          }
-        } else if constexpr (A::kWords == 1) {
-          if constexpr (LAST) __stcs(reinterpret_cast<unsigned int*>(dst), xr);
-          else __stcg(reinterpret_cast<unsigned int*>(dst), xr);
-        } else {
-          if constexpr (LAST) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
-          else __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
-        }
-      }
+    mp_tile<S1, A, STANDARD, FIRST, CONJ_IN, SCALE_OUT, LAST, BOUT>(
+        buf, tw_base, reinterpret_cast<const uint8_t*>(p.tw), p.scale, P, N, q, rb, second, g,
+        warp, lane, [&] { return p.out + b * N * EB; },  // == pair b/2 * N * 8 for packed pairs
+        release, [] {});
   };
 
   if constexpr (FIRST) {
@@ -414,23 +210,6 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-struct MpGroup {
-  int P, s;
-  uint4* d_tw = nullptr;
-};
-
-struct MultipassPlan {
-  int m = 0, strategy = 0, precision = 0, sm_count = 0;
-  bool f16_pairs = true;  // fp16 value layout: transform pairs (else one complex/register)
-  size_t smem_optin = 0;
-  std::vector<MpGroup> groups;
-  size_t chunk_transforms = 0;
-  ~MultipassPlan() {
-    for (auto& g : groups)
-      if (g.d_tw) cudaFree(g.d_tw);
-  }
-};
-
 namespace {
 
 EncodeFn encode_fn() {
@@ -476,6 +255,13 @@ std::vector<int> split_passes(int m, int max_s) {
 
 size_t sample_bytes(int precision) { return precision == kFp16 ? 4 : 8; }
 
+}  // namespace
+
+int env_or(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 // Input map of a pass group over `batch` transforms starting at `base`.
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
                 long long batch) {
@@ -512,6 +298,9 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
   }
   return int(r);
 }
+
+
+namespace {
 
 template <int S1, class A, bool STD>
 cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, bool conj_in,
@@ -591,9 +380,18 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   const char* lay = std::getenv("DSFFT_MP_F16_LAYOUT");
   mp->f16_pairs = !(lay && std::atoi(lay) == 2);
   const bool f16c = precision == kFp16 && !mp->f16_pairs;
+  // one launch, L2-resident intermediate (multipass_fused.cu): m = 2s with s
+  // in 7..9 (N = 2^14, 2^16, 2^18), two-word values (fp32, fp16 transform
+  // pairs).  Opt-in (DSFFT_MP_FUSED=1): it moves 1.01x the algorithmic DRAM
+  // bytes (vs 2x) and stays under the board power cap, but with two
+  // 256-thread tile groups per SM (128 registers, ~200 KB smem) it is bound by
+  // SM latency, and measures 0.85-1.12x the two-launch path (profiles/).
+  mp->fused = !f16c && m % 2 == 0 && m >= 14 && m <= 18 && env_or("DSFFT_MP_FUSED", 0) != 0;
   auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
   int P = 0;
-  for (int s : split_passes(m, 9)) {
+  const std::vector<int> split =
+      mp->fused ? std::vector<int>{m / 2, m / 2} : split_passes(m, 9);
+  for (int s : split) {
     MpGroup g;
     g.P = P;
     g.s = s;
@@ -660,6 +458,7 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const bool f16 = mp.precision == kFp16;
   const bool std_ = mp.strategy == kStandard;
   const int ng = int(mp.groups.size());
+  if (mp.fused) return fused_execute(mp, inverse, in, out, batch, scale, stream, launches);
   // per-call, stream-ordered intermediates (plans may run on several streams)
   const size_t chunk = std::min(mp.chunk_transforms, batch);
   uint8_t* scratch[2] = {nullptr, nullptr};

@@ -96,6 +96,31 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- inter-CTA flags (gpu scope) ---------------------------------------------
+// Producer: after the data stores of the whole tile group (bar.sync), one
+// thread publishes with a release add; consumer: acquire load spin.
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_at_least(const uint32_t* p, uint32_t want) {
+  // counters only grow; a wrap-safe comparison keeps long runs correct
+  while (int32_t(ld_acquire(p) - want) < 0) __nanosleep(64);
+}
+// Drop a 128-byte global line from L2 WITHOUT writing it back (its data is
+// dead: a consumed scratch intermediate), so dirty scratch never reaches HBM.
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+// Generic-proxy global writes / reads vs async-proxy (TMA) accesses.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ---- barriers ---------------------------------------------------------------
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

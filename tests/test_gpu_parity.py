@@ -439,3 +439,44 @@ def test_config5_size_properties(dsfft, cuda, orc, n, precision, sample):
     rep = dsfft.error_device(plan, x, metric)
     assert rep["trials"] == batch and rep["nonfinite_trials"] == 0
     assert rep["rel_l2_max"] < (5e-6 if precision == "fp32" else (1 + 2.0 ** -11) ** 16 - 1)
+
+
+@pytest.mark.parametrize("n", [1 << 14, 1 << 16, 1 << 18])
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+@pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
+def test_fused_multipass_bit_exact(dsfft, cuda, orc, monkeypatch, n, precision, inverse):
+    """The one-launch path (DSFFT_MP_FUSED=1, multipass_fused.cu): odd batch
+    (a half-empty last fp16 pair), every strategy with a butterfly of its own."""
+    monkeypatch.setenv("DSFFT_MP_FUSED", "1")
+    chk = _checker()
+    batch = 5 if n <= 1 << 16 else 3
+    x = ref_inputs(orc, n, batch, seed=n + 17, precision=precision)
+    for s in ("dual", "standard"):
+        plan = dsfft.make_plan(n, s, precision)
+        y = _device_run(dsfft, cuda, plan, to_work(x, precision), inverse)
+        want = to_work((chk.inverse if inverse else chk.forward)(x, s, precision), precision)
+        assert bit_mismatches(y, want) == 0, (n, s, precision, inverse)
+        assert dsfft.last_launch_count() == 1
+
+
+@pytest.mark.parametrize("lag,slots,teams", [(1, None, None), (2, None, 3), (1, 4, 1)])
+def test_fused_multipass_slot_reuse(dsfft, cuda, orc, monkeypatch, lag, slots, teams):
+    """Many units per team: scratch slots are reused for several generations
+    (done / freed counters), with different lags, ring sizes and team counts;
+    in place.  Sampled transforms against the reference."""
+    monkeypatch.setenv("DSFFT_MP_FUSED", "1")
+    monkeypatch.setenv("DSFFT_FUSED_LAG", str(lag))
+    if slots:
+        monkeypatch.setenv("DSFFT_FUSED_SLOTS", str(slots))
+    if teams:
+        monkeypatch.setenv("DSFFT_FUSED_TEAMS", str(teams))
+    chk = _checker()
+    n, batch = 1 << 14, 301
+    x = ref_inputs(orc, n, batch, seed=99 + lag, precision="fp16")
+    plan = dsfft.make_plan(n, "dual", "fp16")
+    t = cuda.from_numpy(to_work(x, "fp16")).cuda()
+    dsfft.forward(plan, t, out=t)  # in place
+    cuda.cuda.synchronize()
+    idx = np.array([0, 1, 2, 77, 150, 151, 298, 299, 300])
+    want = to_work(chk.forward(x[idx], "dual", "fp16"), "fp16")
+    assert bit_mismatches(t.cpu().numpy()[idx], want) == 0

@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 for spec in "$@"; do
   label=${spec%%:*}
   args=${spec#*:}
-  cmd="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-accuracy $args"
+  cmd="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-accuracy --sustained-seconds 0 $args"
   if timeout 300 $cmd > "gpurun_out/plain_$label.log" 2>&1; then
     timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${KREGEX:-fft_small}" \
       -s "${SKIP:-3}" -c "${COUNT:-1}" -o "gpurun_out/prof_$label" -f $cmd > "gpurun_out/ncu_$label.log" 2>&1
