@@ -242,9 +242,12 @@ std::vector<int> split_passes(int m, int max_s) {
     }
     if (ok && sum == m && v.size() >= 2) return v;
   }
-  // 2 groups up to m = 2*max_s, 3 beyond; every group 6..max_s passes
-  // (max_s = 9 for one-word fp16 values, 8 for fp32: a 2-deep ring of
-  // 32 x 2^s x 8-byte tiles must fit in shared memory)
+  // 2 groups up to m = 2*max_s, 3 beyond; every group 6..max_s passes.
+  // max_s = 9 for every value width: at 8-byte values (fp32, fp16 pairs) an
+  // s = 9 tile is 128 KiB, so mp_launch_t falls back to one 1-deep tile group
+  // per CTA there (m = 17, 18); the 3-group split that max_s = 8 would force
+  // instead measured within +-3% (profiles/r01_sweep.md) and
+  // costs a third HBM round trip.
   if (m <= 2 * max_s) {
     const int a = (m + 1) / 2;
     return {a, m - a};

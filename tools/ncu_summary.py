@@ -90,9 +90,10 @@ def main():
     ap.add_argument("--sample-bytes", type=int, default=4)
     ap.add_argument("--round", default="r01")
     ap.add_argument("--launches", default=None)
+    ap.add_argument("--kernel", default="fft", help="substring of the captured kernel's name")
     a = ap.parse_args()
     ms = raw_metrics(a.rep)
-    k = [m for m in ms if "fft" in m["kernel"]][0]
+    k = [m for m in ms if a.kernel in m["kernel"]][0]
     rd = to_bytes(*k["dram__bytes_read.sum"])
     wr = to_bytes(*k["dram__bytes_write.sum"])
     dur = to_ms(*k["gpu__time_duration.sum"])
