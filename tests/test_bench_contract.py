@@ -33,3 +33,28 @@ def test_reference_arm_json_line(orc, ref):
     e = d["e2e"]
     assert e["value"] == d["value"] and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_flag_self_launches_torchrun():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under
+    torch.distributed.run with 2 ranks, passing every flag through (including
+    ones torchrun's own parser would mistake, like --n).  Without a GPU each
+    rank must then stop at the device check -- never at argument parsing."""
+    import pytest
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--n",
+                        "1024", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0
+    out = r.stdout + r.stderr
+    assert "ambiguous option" not in out and "unrecognized arguments" not in out, out[-2000:]
+    assert out.count("bench.py: no CUDA device") == 2, out[-2000:]
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=3" in r.stderr

@@ -13,16 +13,20 @@ for n in $NS; do
     sb=$([ "$p" = fp16 ] && echo 4 || echo 8)
     batch=$(( (4 << 30) / (n * sb) ))  # >= 4 GiB of input
     for s in ${STRATS:-standard lf cosine dual}; do
+      # the reference's CPU path beside it (dual only, a 3 s sample on all cores)
+      cpu=$([ "$s" = dual ] && echo "--cpu-seconds 3" || echo "--no-cpu")
       timeout 300 python bench.py --n "$n" --precision "$p" --strategy "$s" --steps "${STEPS:-30}" \
-        --warmup 3 --batch "$batch" --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
+        --warmup 3 --batch "$batch" $cpu --no-e2e --no-accuracy --sustained-seconds 0 \
+        2>/dev/null | tail -1 >> "$out"
     done
   done
 done
 for n in $LARGE; do
   for p in fp16 fp32; do
     for s in ${LSTRATS:-standard dual}; do
+      cpu=$([ "$s" = dual ] && echo "--cpu-seconds 3" || echo "--no-cpu")
       timeout 300 python bench.py --n "$n" --precision "$p" --strategy "$s" --steps "${STEPS:-30}" \
-        --warmup 3 --no-cpu --no-e2e --no-accuracy 2>/dev/null | tail -1 >> "$out"
+        --warmup 3 $cpu --no-e2e --no-accuracy --sustained-seconds 0 2>/dev/null | tail -1 >> "$out"
     done
   done
 done

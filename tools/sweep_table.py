@@ -17,8 +17,8 @@ def main(path):
     ns = sorted({k[0] for k in table})
     strats = [s for s in ("standard", "lf", "cosine", "dual") if any(k[2] == s for k in table)]
     clocks = sorted({d.get("clocks", {}).get("sm_mhz") for d in rows} - {None})
-    print("| N | precision | " + " | ".join(strats) + " |")
-    print("|---|---|" + "---|" * len(strats))
+    print("| N | precision | " + " | ".join(strats) + " | reference CPU, dual (16 cores) | GPU / CPU |")
+    print("|---|---|" + "---|" * len(strats) + "---|---|")
     for n in ns:
         for p in ("fp16", "fp32"):
             cells = []
@@ -28,6 +28,12 @@ def main(path):
                     cells.append("")
                     continue
                 cells.append(f"{100 * d['roofline']['frac']:.1f}% ({d['value'] / 1e6:.1f} M/s)")
+            ref = table.get((n, p, "dual"), {}).get("cpu_baseline") or {}
+            if ref.get("value"):
+                g = table[(n, p, "dual")]["value"]
+                cells += [f"{ref['value']:.3g} /s ({ref.get('kind')})", f"{g / ref['value']:.3g}x"]
+            else:
+                cells += ["", ""]
             if any(cells):
                 print(f"| {n} | {p} | " + " | ".join(cells) + " |")
     print()
