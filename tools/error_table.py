@@ -63,10 +63,13 @@ def main():
         for n, p, s, trials, r in rows:
             eps = 2.0 ** -11 if p == "fp16" else 2.0 ** -24
             b = bound(n, s, eps) if s != "standard" else float("nan")
+            per = t_max(n, s) * eps  # per_butterfly_bound; divergent when >= 1
             ok = "-" if s == "standard" or not math.isfinite(b) else \
                 ("yes" if r["rel_l2_max"] <= b else
                  ("non-finite, as the reference (k=N/4 singular ratio)"
-                  if s == "cosine" and not math.isfinite(r["rel_l2_max"]) else "NO"))
+                  if s == "cosine" and not math.isfinite(r["rel_l2_max"]) else
+                  (f"non-finite, as the reference (divergent: per-butterfly bound {per:.3g} >= 1)"
+                   if per >= 1 and not math.isfinite(r["rel_l2_max"]) else "NO")))
             f.write(f"| {n} | {p} | {s} | {trials} | {r['rel_l2_median']:.3e} | "
                     f"{r['rel_l2_max']:.3e} | {r['nonfinite_trials']} | {b:.3e} | {ok} |\n")
         du = {(n, p): r for n, p, s, _, r in rows if s == "dual"}
