@@ -442,20 +442,6 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
     mp->groups.push_back(g);
     P += s;
   }
-  // N = 2^16 (8 + 8): the warp-independent one-launch kernel needs its
-  // quad-ordered second-group slab (multipass_quad.cu); DSFFT_MP_QUAD=0 keeps
-  // the 8-warp tile kernel
-  if (mp->fused && m == 16 && env_or("DSFFT_MP_QUAD", 1) != 0) {
-    const std::vector<uint8_t> img = serialize_records(
-        quad_slab_records(table, m, strategy, precision), record_bytes(precision, false));
-    if (cudaMalloc(&mp->d_tw_quad, img.size()) != cudaSuccess ||
-        cudaMemcpy(mp->d_tw_quad, img.data(), img.size(), cudaMemcpyHostToDevice) !=
-            cudaSuccess) {
-      g_mp_err = "multipass: twiddle upload failed";
-      delete mp;
-      return nullptr;
-    }
-  }
   // chunk so the intermediate (one scratch buffer) stays L2-resident
   const size_t tb = (size_t(1) << m) * sample_bytes(precision);
   const char* env = std::getenv("DSFFT_MP_CHUNK_MB");

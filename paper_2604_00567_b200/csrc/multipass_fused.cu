@@ -38,6 +38,19 @@ namespace dsfft {
 // Progress: every wait is on an item earlier in the same per-group sequence
 // of another team member, and the launch is cooperative (all CTAs
 // co-resident), so the earliest unfinished item can always run.
+struct FusedParams {
+  uint8_t* out;        // user output (batch base)
+  uint8_t* mid;        // scratch: teams * R unit slots (blocked, pair-packed)
+  const uint4* twA;    // first-group records (mp_first_records)
+  const uint4* twB;    // second-group records, K column blocks of mp_block_records
+  uint32_t* done;      // [teams * R] first-group tiles stored into the slot (monotonic)
+  uint32_t* freed;     // [teams * R] second-group tiles that read the slot (monotonic)
+  int m, s;            // log2 N = 2 s
+  int K, teams, R, D;  // team size, teams, scratch slots per team, lag in units per group
+  long long nb;        // transforms
+  long long units;     // ceil(nb / PAIR)
+  uint32_t scale;
+};
 
 template <int S1, class A, bool STANDARD, bool INVERSE, int MAXT, int SLAB>
 __global__ void __launch_bounds__(MAXT, 1)
@@ -258,17 +271,8 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
   const bool std_ = mp.strategy == kStandard;
   const int s = mp.m / 2, S1 = s - 5;
   const long long units = f16 ? (long long)(batch + 1) / 2 : (long long)batch;
-  const bool quad = mp.d_tw_quad != nullptr;
-  FusedShape f = f16 ? fused_shape_a<ArithF16P>(S1, mp.m, mp.sm_count, mp.smem_optin, units)
-                     : fused_shape_a<ArithF32>(S1, mp.m, mp.sm_count, mp.smem_optin, units);
-  if (quad && f.K) {  // two unit streams of 8 warps (quads) per CTA
-    f.G = 2;
-    f.D = std::max(1, env_or("DSFFT_FUSED_LAG", 1));
-    f.R = std::max(4, env_or("DSFFT_FUSED_SLOTS", 2 * (f.D + 2)));
-    f.R = (f.R + 1) / 2 * 2;
-    f.smem = quad_smem_bytes(mp.precision);
-    if (f.smem > mp.smem_optin) f.K = 0;
-  }
+  const FusedShape f = f16 ? fused_shape_a<ArithF16P>(S1, mp.m, mp.sm_count, mp.smem_optin, units)
+                           : fused_shape_a<ArithF32>(S1, mp.m, mp.sm_count, mp.smem_optin, units);
   if (f.K == 0) {
     set_mp_error("multipass: fused kernel does not fit");
     return 1;
@@ -292,12 +296,19 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
     set_mp_error("multipass: flag reset failed");
     return 1;
   }
+  CUtensorMap in_map, mid_map;
+  int rc = make_in_map(&in_map, in, mp.m, 0, s, f16 ? 4 : 8, (long long)batch);
+  if (!rc) rc = make_in_map(&mid_map, scratch, mp.m, s, s, 8, (long long)slots);
+  if (rc) {
+    set_mp_error("multipass: cuTensorMapEncodeTiled failed (fused, CUresult " +
+                 std::to_string(rc) + ")");
+    return 1;
+  }
   FusedParams p{};
-  p.in = static_cast<const uint8_t*>(in);
   p.out = static_cast<uint8_t*>(out);
   p.mid = scratch;
   p.twA = mp.groups[0].d_tw;
-  p.twB = quad ? mp.d_tw_quad : mp.groups[1].d_tw;
+  p.twB = mp.groups[1].d_tw;
   p.done = flags;
   p.freed = flags + slots;
   p.m = mp.m;
@@ -309,23 +320,6 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
   p.nb = (long long)batch;
   p.units = units;
   p.scale = scale;
-  if (quad) {
-    const cudaError_t e = quad_launch(p, mp.precision, std_, inverse, f.teams * f.K, stream);
-    if (e != cudaSuccess) {
-      set_mp_error(std::string("mp_quad_kernel launch: ") + cudaGetErrorString(e));
-      return 1;
-    }
-    if (launches) ++*launches;
-    return 0;
-  }
-  CUtensorMap in_map, mid_map;
-  int rc = make_in_map(&in_map, in, mp.m, 0, s, f16 ? 4 : 8, (long long)batch);
-  if (!rc) rc = make_in_map(&mid_map, scratch, mp.m, s, s, 8, (long long)slots);
-  if (rc) {
-    set_mp_error("multipass: cuTensorMapEncodeTiled failed (fused, CUresult " +
-                 std::to_string(rc) + ")");
-    return 1;
-  }
   cudaError_t e;
   if (f16)
     e = std_ ? fused_launch_a<ArithF16P, true>(S1, in_map, mid_map, p, f, inverse, stream)
