@@ -480,3 +480,21 @@ def test_fused_multipass_slot_reuse(dsfft, cuda, orc, monkeypatch, lag, slots, t
     idx = np.array([0, 1, 2, 77, 150, 151, 298, 299, 300])
     want = to_work(chk.forward(x[idx], "dual", "fp16"), "fp16")
     assert bit_mismatches(t.cpu().numpy()[idx], want) == 0
+
+
+def test_execute_validates_out(dsfft, cuda):
+    """`out` must match the input exactly (advisor finding: a short or
+    mistyped `out` would otherwise be written out of bounds)."""
+    torch = cuda
+    plan = dsfft.make_plan(1024, "dual", "fp16")
+    x = torch.zeros((4, 1024, 2), dtype=torch.float16, device="cuda")
+    for bad in (torch.zeros((3, 1024, 2), dtype=torch.float16, device="cuda"),
+                torch.zeros((4, 1024, 2), dtype=torch.float32, device="cuda"),
+                torch.zeros((4, 2, 1024), dtype=torch.float16, device="cuda").transpose(1, 2),
+                torch.zeros((4, 1024, 2), dtype=torch.float16)):
+        with pytest.raises(ValueError):
+            dsfft.forward(plan, x, out=bad)
+    with pytest.raises(ValueError):
+        dsfft.forward(dsfft.make_plan(512, "dual", "fp16"), x)
+    with pytest.raises(ValueError):
+        dsfft.error_device(plan, x, reference="nope")
