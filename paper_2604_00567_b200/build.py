@@ -54,8 +54,8 @@ def jobs():
         src = os.path.join(CSRC, "inst_small.cu")
         obj = os.path.join(OBJ, f"inst_m{m}.o")
         out.append((obj, [src] + hdr, [NVCC] + NVFLAGS + [f"-DDSFFT_M={m}", "-c", src, "-o", obj]))
-    for name in ("dsfft_capi.cu", "multipass.cu", "multipass_fused.cu", "multipass_octet.cu",
-                 "fp64.cu", "error_harness.cu", "synth.cu"):
+    for name in ("dsfft_capi.cu", "multipass.cu", "multipass_fused.cu", "fp64.cu", "error_harness.cu",
+                 "synth.cu"):
         src = os.path.join(CSRC, name)
         obj = os.path.join(OBJ, name.replace(".cu", ".o"))
         out.append((obj, [src] + hdr, [NVCC] + NVFLAGS + ["-c", src, "-o", obj]))

@@ -267,7 +267,7 @@ int env_or(const char* name, int dflt) {
 
 // Input map of a pass group over `batch` transforms starting at `base`.
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
-                long long batch, int box_cols) {
+                long long batch) {
   EncodeFn enc = encode_fn();
   if (!enc) return -1;
   const CUtensorMapDataType dt =
@@ -279,14 +279,14 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
   if (P == 0) {  // {q (N/2^s), c (2^s), b}
     cuuint64_t dims[3] = {N >> s, cuuint64_t(1) << s, cuuint64_t(batch)};
     cuuint64_t strides[2] = {(N >> s) * vb, N * vb};
-    cuuint32_t box[3] = {cuuint32_t(box_cols), rows_box, 1};
+    cuuint32_t box[3] = {32, rows_box, 1};
     r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (P + s == m) {  // last group: blocked intermediate {r_l, c, rb, b}
     cuuint64_t dims[4] = {32, cuuint64_t(1) << s, N >> (s + 5), cuuint64_t(batch)};
     cuuint64_t strides[3] = {32 * cuuint64_t(vb), (cuuint64_t(32) << s) * vb, N * vb};
-    cuuint32_t box[4] = {cuuint32_t(box_cols), rows_box, 1, 1};
+    cuuint32_t box[4] = {32, rows_box, 1, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -294,7 +294,7 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
     cuuint64_t dims[4] = {cuuint64_t(1) << P, N >> (P + s), cuuint64_t(1) << s,
                           cuuint64_t(batch)};
     cuuint64_t strides[3] = {(cuuint64_t(1) << P) * vb, (N >> s) * vb, N * vb};
-    cuuint32_t box[4] = {cuuint32_t(box_cols), 1, rows_box, 1};
+    cuuint32_t box[4] = {32, 1, rows_box, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -441,20 +441,6 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
     }
     mp->groups.push_back(g);
     P += s;
-  }
-  // N = 2^16 (8 + 8): the 2-warp-group one-launch kernel needs its
-  // octet-ordered second-group slab (multipass_octet.cu); DSFFT_MP_OCTET=0
-  // keeps the 8-warp tile kernel
-  if (mp->fused && m == 16 && env_or("DSFFT_MP_OCTET", 1) != 0) {
-    const std::vector<uint8_t> img = serialize_records(
-        octet_slab_records(table, m, strategy, precision), record_bytes(precision, false));
-    if (cudaMalloc(&mp->d_tw_oct, img.size()) != cudaSuccess ||
-        cudaMemcpy(mp->d_tw_oct, img.data(), img.size(), cudaMemcpyHostToDevice) !=
-            cudaSuccess) {
-      g_mp_err = "multipass: twiddle upload failed";
-      delete mp;
-      return nullptr;
-    }
   }
   // chunk so the intermediate (one scratch buffer) stays L2-resident
   const size_t tb = (size_t(1) << m) * sample_bytes(precision);

@@ -38,6 +38,19 @@ namespace dsfft {
 // Progress: every wait is on an item earlier in the same per-group sequence
 // of another team member, and the launch is cooperative (all CTAs
 // co-resident), so the earliest unfinished item can always run.
+struct FusedParams {
+  uint8_t* out;        // user output (batch base)
+  uint8_t* mid;        // scratch: teams * R unit slots (blocked, pair-packed)
+  const uint4* twA;    // first-group records (mp_first_records)
+  const uint4* twB;    // second-group records, K column blocks of mp_block_records
+  uint32_t* done;      // [teams * R] first-group tiles stored into the slot (monotonic)
+  uint32_t* freed;     // [teams * R] second-group tiles that read the slot (monotonic)
+  int m, s;            // log2 N = 2 s
+  int K, teams, R, D;  // team size, teams, scratch slots per team, lag in units per group
+  long long nb;        // transforms
+  long long units;     // ceil(nb / PAIR)
+  uint32_t scale;
+};
 
 template <int S1, class A, bool STANDARD, bool INVERSE, int MAXT, int SLAB>
 __global__ void __launch_bounds__(MAXT, 1)
@@ -283,11 +296,9 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
     set_mp_error("multipass: flag reset failed");
     return 1;
   }
-  const bool octet = mp.d_tw_oct != nullptr && octet_smem_bytes(mp.precision) <= mp.smem_optin;
   CUtensorMap in_map, mid_map;
-  const int box = octet ? 8 : 32;  // octet tiles load 8-column boxes
-  int rc = make_in_map(&in_map, in, mp.m, 0, s, f16 ? 4 : 8, (long long)batch, box);
-  if (!rc) rc = make_in_map(&mid_map, scratch, mp.m, s, s, 8, (long long)slots, box);
+  int rc = make_in_map(&in_map, in, mp.m, 0, s, f16 ? 4 : 8, (long long)batch);
+  if (!rc) rc = make_in_map(&mid_map, scratch, mp.m, s, s, 8, (long long)slots);
   if (rc) {
     set_mp_error("multipass: cuTensorMapEncodeTiled failed (fused, CUresult " +
                  std::to_string(rc) + ")");
@@ -310,16 +321,6 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
   p.units = units;
   p.scale = scale;
   cudaError_t e;
-  if (octet) {
-    p.twB = mp.d_tw_oct;
-    e = octet_launch(in_map, mid_map, p, mp.precision, std_, inverse, f.teams * f.K, stream);
-    if (e != cudaSuccess) {
-      set_mp_error(std::string("mp_octet_kernel launch: ") + cudaGetErrorString(e));
-      return 1;
-    }
-    if (launches) ++*launches;
-    return 0;
-  }
   if (f16)
     e = std_ ? fused_launch_a<ArithF16P, true>(S1, in_map, mid_map, p, f, inverse, stream)
              : fused_launch_a<ArithF16P, false>(S1, in_map, mid_map, p, f, inverse, stream);

@@ -253,30 +253,13 @@ struct MultipassPlan {
   int m = 0, strategy = 0, precision = 0, sm_count = 0;
   bool f16_pairs = true;  // fp16 value layout: transform pairs (else one complex/register)
   bool fused = false;     // both pass groups in one launch (mp_fused_kernel)
-  uint4* d_tw_oct = nullptr;  // s = 8: octet slab -> 2-warp-group one-launch kernel
   size_t smem_optin = 0;
   std::vector<MpGroup> groups;
   size_t chunk_transforms = 0;
   ~MultipassPlan() {
     for (auto& g : groups)
       if (g.d_tw) cudaFree(g.d_tw);
-    if (d_tw_oct) cudaFree(d_tw_oct);
   }
-};
-
-// Parameters of the one-launch kernels (multipass_fused.cu, multipass_octet.cu).
-struct FusedParams {
-  uint8_t* out;        // user output (batch base)
-  uint8_t* mid;        // scratch: teams * R unit slots (blocked, pair-packed)
-  const uint4* twA;    // first-group records (mp_first_records)
-  const uint4* twB;    // second-group records, K column blocks of mp_block_records
-  uint32_t* done;      // [teams * R] first-group tiles stored into the slot (monotonic)
-  uint32_t* freed;     // [teams * R] second-group tiles that read the slot (monotonic)
-  int m, s;            // log2 N = 2 s
-  int K, teams, R, D;  // team size, teams, scratch slots per team, lag in units per group
-  long long nb;        // transforms
-  long long units;     // ceil(nb / PAIR)
-  uint32_t scale;
 };
 
 void set_mp_error(const std::string& msg);
@@ -284,19 +267,9 @@ void set_mp_error(const std::string& msg);
 int env_or(const char* name, int dflt);
 // TMA map over `batch` transforms at `base` for pass group [P, P+s) (see multipass.cu)
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
-                long long batch, int box_cols = 32);
-// one-launch execution of an eligible plan (multipass_fused.cu); with an
-// octet slab uploaded (s = 8) it runs the 2-warp-group kernel of
-// multipass_octet.cu
+                long long batch);
+// one-launch execution of an eligible plan (multipass_fused.cu)
 int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, size_t batch,
                   uint32_t scale, cudaStream_t stream, uint64_t* launches);
-// the octet kernel: smem bytes, launch (in_map: user input with 8-column
-// boxes; mid_map: scratch units with 8-column boxes)
-size_t octet_smem_bytes(int precision);
-cudaError_t octet_launch(const CUtensorMap& in_map, const CUtensorMap& mid_map,
-                         const FusedParams& p, int precision, bool standard, bool inverse,
-                         int grid, cudaStream_t stream);
-std::vector<Record> octet_slab_records(const std::vector<TableEntry>& table, int m, int strategy,
-                                       int precision);
 
 }  // namespace dsfft
