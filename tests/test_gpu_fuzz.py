@@ -23,7 +23,7 @@ _MAXM = int(os.environ.get("DSFFT_FUZZ_MAXM", "15"))
 
 
 @pytest.mark.parametrize("case", range(_CASES))
-def test_random_cases(dsfft, cuda, orc, case):
+def test_random_cases(dsfft, cuda, orc, monkeypatch, case):
     torch = cuda
     rng = np.random.RandomState(_SEED + case)
     m = int(rng.choice(list(range(1, 16)) + list(range(16, _MAXM + 1))))
@@ -34,6 +34,8 @@ def test_random_cases(dsfft, cuda, orc, case):
     in_place = bool(rng.randint(2))
     max_batch = max(1, (1 << 17) >> m)
     batch = int(rng.randint(1, max_batch + 1))
+    # half the large-N plans take the one-launch path (DSFFT_MP_FUSED, opt-in)
+    monkeypatch.setenv("DSFFT_MP_FUSED", str(int(rng.randint(2))))
     x = ref_inputs(orc, n, batch, seed=case, precision=precision)
     xw = x if precision == "fp64" else to_work(x, precision)
     plan = dsfft.make_plan(n, strategy, precision)
