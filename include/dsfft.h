@@ -228,6 +228,26 @@ int dsfft_fill_uniform(void* d_out, size_t n, uint64_t first_transform, size_t c
 int dsfft_round_to(const double* in, void* out, size_t count, int precision);
 int dsfft_widen(const void* in, double* out, size_t count, int precision);
 
+/* The reference's scalar precision model, ArithmeticContext::add / sub / mul
+ * / fma (precision.cpp:77-111), evaluated on `device` elementwise over host
+ * arrays: out[i] = op(a[i], b[i] [, c[i]]) with op DSFFT_OP_*, rounded exactly
+ * as the context rounds (fp16: the double result rounded to binary16 with
+ * round_to's overflow rule; fp32: the operation on the float-cast operands;
+ * fp64: the double operation), for any double inputs.  `c` is read for FMA
+ * only. */
+enum { DSFFT_OP_ADD = 0, DSFFT_OP_SUB = 1, DSFFT_OP_MUL = 2, DSFFT_OP_FMA = 3 };
+int dsfft_context_ops(int precision, int op, const double* a, const double* b, const double* c,
+                      double* out, size_t count, int device);
+
+/* The butterfly-variant API (butterfly.hpp:22-61: butterfly_standard /
+ * _linzer_feig / _cosine / _dual, selected like kernel_for(strategy)) on
+ * `device`, batched: for each i, the variant's butterfly of a[2i..2i+1],
+ * b[2i..2i+1] (re, im) with table entry entries[i] under `precision`'s
+ * rounding; out[4i..4i+3] = sum.re, sum.im, diff.re, diff.im.  Bit-identical
+ * to the reference for any double inputs. */
+int dsfft_butterflies(int strategy, int precision, const double* a, const double* b,
+                      const dsfft_entry* entries, double* out, size_t count, int device);
+
 /* Bytes of one complex sample in the working precision (4, 8), 0 if invalid. */
 size_t dsfft_sample_bytes(int precision);
 

@@ -79,6 +79,7 @@ class CpuFft:
                                 C.c_int, C.POINTER(Counters)]
         f("butterfly").argtypes = [C.c_int, C.c_int, _DP, _DP, C.POINTER(Entry), _DP,
                                    C.POINTER(Counters)]
+        f("ctx_op").argtypes = [C.c_int, C.c_int, _DP, _DP, _DP, _DP, C.c_size_t]
         f("rel_l2").restype = C.c_double
         f("rel_l2").argtypes = [_DP, _DP, C.c_size_t]
         f("cumulative_bound").restype = C.c_double
@@ -159,6 +160,16 @@ class CpuFft:
                                          np.array([b.real, b.imag]), C.byref(e), out,
                                          C.byref(cnt)))
         return complex(out[0], out[1]), complex(out[2], out[3]), cnt
+
+    def ctx_op(self, precision: str, op: str, a, b, c=None):
+        """ArithmeticContext::add/sub/mul/fma elementwise (precision.cpp:77-111)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        c = np.ascontiguousarray(c if c is not None else np.zeros_like(a), dtype=np.float64)
+        out = np.empty_like(a)
+        self._f("ctx_op")(PRECISIONS[precision], ("add", "sub", "mul", "fma").index(op), a, b, c,
+                          out, a.size)
+        return out
 
     def dft(self, x):
         x = np.ascontiguousarray(x, dtype=np.complex128)

@@ -95,6 +95,19 @@ static double ctx_fma(ctx_t* cx, double a, double b, double c) { /* precision.cp
 
 /* ---- twiddle.cpp -------------------------------------------------------- */
 
+/* the context operations elementwise (op 0 add, 1 sub, 2 mul, 3 fma) */
+void orc_ctx_op(int p, int op, const double* a, const double* b, const double* c, double* out,
+                size_t count) {
+  ctx_t cx;
+  memset(&cx, 0, sizeof cx);
+  cx.p = p;
+  for (size_t i = 0; i < count; ++i)
+    out[i] = op == 0 ? ctx_add(&cx, a[i], b[i])
+           : op == 1 ? ctx_sub(&cx, a[i], b[i])
+           : op == 2 ? ctx_mul(&cx, a[i], b[i])
+                     : ctx_fma(&cx, a[i], b[i], c[i]);
+}
+
 static int check_size(size_t n) { /* twiddle.cpp:14-18 */
   if (n < 2 || (n & (n - 1)) != 0) {
     snprintf(g_err, sizeof g_err, "FFT size must be a power of two >= 2, got %zu", n);

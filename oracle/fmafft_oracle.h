@@ -88,6 +88,9 @@ int orc_inverse(size_t n, int strategy, int precision, const double* in,
 int orc_butterfly(int strategy, int precision, const double a[2],
                   const double b[2], const orc_entry* e, double out[4],
                   orc_counters* counters);
+/* ArithmeticContext::add / sub / mul / fma (op 0..3, precision.cpp:77-111), elementwise */
+void orc_ctx_op(int p, int op, const double* a, const double* b, const double* c, double* out,
+                size_t count);
 
 void orc_dft(size_t n, const double* in, double* out, size_t batch, int threads);
 /* +inf when x holds a non-finite component; NaN on length/zero-ref error. */

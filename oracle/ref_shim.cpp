@@ -169,6 +169,17 @@ int ref_butterfly(int s, int p, const double a[2], const double b[2],
   });
 }
 
+// ArithmeticContext::add/sub/mul/fma (op 0..3) of a fresh context, elementwise
+void ref_ctx_op(int p, int op, const double* a, const double* b, const double* c, double* out,
+                std::size_t count) {
+  fmafft::ArithmeticContext ctx(P(p));
+  for (std::size_t i = 0; i < count; ++i)
+    out[i] = op == 0 ? ctx.add(a[i], b[i])
+           : op == 1 ? ctx.sub(a[i], b[i])
+           : op == 2 ? ctx.mul(a[i], b[i])
+                     : ctx.fma(a[i], b[i], c[i]);
+}
+
 void ref_dft(std::size_t n, const double* in, double* out, std::size_t batch) {
   fmafft::SampleBuffer x(n);
   for (std::size_t b = 0; b < batch; ++b) {

@@ -24,7 +24,7 @@ import numpy as np
 __all__ = ["Strategy", "Precision", "FftPlan", "make_plan", "forward", "inverse",
            "execute", "forward_f64", "inverse_f64", "execute_host", "execute_multi",
            "round_to", "widen", "build_table", "table_csv", "bounds_csv", "error_device",
-           "measure_error", "dft_oracle", "dft_device", "make_plan_from_table", "fill_uniform", "synthetic_batch",
+           "measure_error", "dft_oracle", "dft_device", "make_plan_from_table", "fill_uniform", "synthetic_batch", "context_op", "butterflies",
            "last_launch_count", "parse_strategy", "parse_precision", "library_path",
            "DsfftError"]
 
@@ -443,6 +443,48 @@ def synthetic_batch(n: int, first_transform: int, count: int, seed: int, precisi
         parse_precision(precision)]
     out = torch.empty((count, n, 2), dtype=dt, device=torch.device("cuda", device))
     return fill_uniform(out, n, first_transform, seed, precision, stream)
+
+
+_OPS = {"add": 0, "sub": 1, "mul": 2, "fma": 3}
+
+
+def context_op(precision: str, op: str, a, b, c=None, device: int = 0) -> np.ndarray:
+    """ArithmeticContext::add/sub/mul/fma (precision.cpp:77-111) elementwise on
+    the device, rounded exactly as the reference rounds (dsfft_context_ops)."""
+    if op not in _OPS:
+        raise ValueError(f"unknown operation: {op}")
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    c = np.ascontiguousarray(c if c is not None else np.zeros_like(a), dtype=np.float64)
+    if not (a.shape == b.shape == c.shape):
+        raise ValueError("operand shapes differ")
+    out = np.empty_like(a)
+    lib = _load()
+    lib.dsfft_context_ops.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_size_t, C.c_int]
+    _check(lib.dsfft_context_ops(PRECISIONS[parse_precision(precision)], _OPS[op], a.ctypes.data,
+                                 b.ctypes.data, c.ctypes.data, out.ctypes.data, a.size,
+                                 int(device)))
+    return out
+
+
+def butterflies(strategy: str, precision: str, a, b, entries, device: int = 0):
+    """The butterfly-variant API (butterfly.hpp:22-61) on the device: complex128
+    arrays a, b and an ENTRY_DTYPE array of table entries -> (sum, diff)."""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    e = np.ascontiguousarray(entries, dtype=ENTRY_DTYPE)
+    if not (a.shape == b.shape == e.shape):
+        raise ValueError("operand shapes differ")
+    out = np.empty(a.shape + (2,), dtype=np.complex128)
+    lib = _load()
+    lib.dsfft_butterflies.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_size_t, C.c_int]
+    _check(lib.dsfft_butterflies(STRATEGIES[parse_strategy(strategy)],
+                                 PRECISIONS[parse_precision(precision)], a.ctypes.data,
+                                 b.ctypes.data, e.ctypes.data, out.ctypes.data, a.size,
+                                 int(device)))
+    return out[..., 0], out[..., 1]
 
 
 def dft_oracle(x, device: int = 0) -> np.ndarray:

@@ -55,7 +55,7 @@ def jobs():
         obj = os.path.join(OBJ, f"inst_m{m}.o")
         out.append((obj, [src] + hdr, [NVCC] + NVFLAGS + [f"-DDSFFT_M={m}", "-c", src, "-o", obj]))
     for name in ("dsfft_capi.cu", "multipass.cu", "multipass_fused.cu", "fp64.cu", "error_harness.cu",
-                 "synth.cu"):
+                 "synth.cu", "emulate.cu"):
         src = os.path.join(CSRC, name)
         obj = os.path.join(OBJ, name.replace(".cu", ".o"))
         out.append((obj, [src] + hdr, [NVCC] + NVFLAGS + ["-c", src, "-o", obj]))

@@ -15,6 +15,7 @@
 
 #include "../../include/dsfft.h"
 #include "host_table.hpp"
+#include "emulate.cuh"
 #include "error_harness.cuh"
 #include "fp64.cuh"
 #include "multipass.cuh"
@@ -847,6 +848,101 @@ int dsfft_fill_uniform(void* d_out, size_t n, uint64_t first_transform, size_t c
     return cuda_fail(cudaGetLastError(), "fill_uniform launch");
   g_launches = 1;
   return DSFFT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Host arrays -> device, one emulation kernel, results back (synchronous).
+template <class Launch>
+int emulate_call(int device, size_t in_bytes, const void* const* ins, int n_in, void* out,
+                 size_t out_bytes, Launch&& launch) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(DSFFT_ERR_NO_DEVICE, "no CUDA device: dsfft has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) return fail(DSFFT_ERR_INVALID, "device ordinal out of range");
+  DeviceGuard guard(device);
+  void* d[4] = {};
+  void* d_out = nullptr;
+  auto cleanup = [&] {
+    for (void* p : d) cudaFree(p);
+    cudaFree(d_out);
+  };
+  int rc = DSFFT_OK;
+  for (int i = 0; i < n_in && !rc; ++i)
+    if (cudaMalloc(&d[i], in_bytes) != cudaSuccess ||
+        cudaMemcpy(d[i], ins[i], in_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail(DSFFT_ERR_CUDA, "emulation: upload failed");
+  if (!rc && cudaMalloc(&d_out, out_bytes) != cudaSuccess)
+    rc = fail(DSFFT_ERR_CUDA, "emulation: device allocation failed");
+  if (!rc && launch(d, d_out)) rc = cuda_fail(cudaGetLastError(), "emulation kernel launch");
+  if (!rc && cudaMemcpy(out, d_out, out_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(DSFFT_ERR_CUDA, "emulation: download failed");
+  cleanup();
+  if (!rc) g_launches = 1;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dsfft_context_ops(int precision, int op, const double* a, const double* b, const double* c,
+                      double* out, size_t count, int device) {
+  g_launches = 0;
+  if (precision < DSFFT_FP16 || precision > DSFFT_FP64)
+    return fail(DSFFT_ERR_INVALID, "unknown precision: " + std::to_string(precision));
+  if (op < DSFFT_OP_ADD || op > DSFFT_OP_FMA) return fail(DSFFT_ERR_INVALID, "unknown operation");
+  if (!a || !b || !out || (op == DSFFT_OP_FMA && !c)) return fail(DSFFT_ERR_INVALID, "null buffer");
+  if (count == 0) return DSFFT_OK;
+  if (count > SIZE_MAX / 8) return fail(DSFFT_ERR_INVALID, "count too large");
+  const size_t bytes = count * sizeof(double);
+  const void* ins[3] = {a, b, op == DSFFT_OP_FMA ? c : a};
+  return emulate_call(device, bytes, ins, 3, out, bytes, [&](void** d, void* o) {
+    return dsfft::launch_context_ops(precision, op, static_cast<const double*>(d[0]),
+                                     static_cast<const double*>(d[1]),
+                                     static_cast<const double*>(d[2]), static_cast<double*>(o),
+                                     (long long)count, nullptr);
+  });
+}
+
+int dsfft_butterflies(int strategy, int precision, const double* a, const double* b,
+                      const dsfft_entry* entries, double* out, size_t count, int device) {
+  g_launches = 0;
+  if (precision < DSFFT_FP16 || precision > DSFFT_FP64)
+    return fail(DSFFT_ERR_INVALID, "unknown precision: " + std::to_string(precision));
+  if (strategy < DSFFT_STANDARD || strategy > DSFFT_DUAL_SELECT)
+    return fail(DSFFT_ERR_INVALID, "unknown strategy");  // kernel_for (butterfly.cpp:82-90)
+  if (!a || !b || !entries || !out) return fail(DSFFT_ERR_INVALID, "null buffer");
+  if (count == 0) return DSFFT_OK;
+  if (count > SIZE_MAX / 64) return fail(DSFFT_ERR_INVALID, "count too large");
+  const size_t cb = count * 2 * sizeof(double);
+  // a, b: count x 16 B (emulate_call); the 40-byte entries go up separately
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(DSFFT_ERR_NO_DEVICE, "no CUDA device: dsfft has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) return fail(DSFFT_ERR_INVALID, "device ordinal out of range");
+  DeviceGuard guard(device);
+  dsfft_entry* d_e = nullptr;
+  if (cudaMalloc(&d_e, count * sizeof(dsfft_entry)) != cudaSuccess ||
+      cudaMemcpy(d_e, entries, count * sizeof(dsfft_entry), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaFree(d_e);
+    return fail(DSFFT_ERR_CUDA, "emulation: upload failed");
+  }
+  const void* ins[2] = {a, b};
+  const int rc = emulate_call(device, cb, ins, 2, out, 2 * cb, [&](void** d, void* o) {
+    return dsfft::launch_butterflies(strategy, precision, static_cast<const double2*>(d[0]),
+                                     static_cast<const double2*>(d[1]), d_e,
+                                     static_cast<double*>(o), (long long)count, nullptr);
+  });
+  cudaFree(d_e);
+  return rc;
 }
 
 int dsfft_dft_oracle(const double* in, double* out, size_t n, size_t batch, int device) {

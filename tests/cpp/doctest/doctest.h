@@ -6,8 +6,8 @@
 // .epsilon() / .scale(), doctest's comparison rule).  With
 // DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN defined before the include it also
 // provides main(): runs every registered case (argv[1], if given, is a
-// substring filter on the case names, or "file:<substring>" on the source
-// file), prints one line per failed assertion
+// comma-separated list of substrings of case names -- or "file:<substring>"
+// on the source file -- and a case runs if any matches), prints one line per failed assertion
 // and a summary, and exits nonzero on any failure.
 //
 // Used to compile the reference's test sources UNMODIFIED against the drop-in
@@ -184,8 +184,17 @@ int main(int argc, char** argv) {
   for (const Case& c : registry()) {
     if (filter && std::strncmp(filter, "file:", 5) == 0) {
       if (!std::strstr(c.file, filter + 5)) continue;
-    } else if (filter && !std::strstr(c.name, filter)) {
-      continue;
+    } else if (filter) {
+      bool hit = false;
+      std::string f(filter);
+      for (size_t at = 0; at <= f.size() && !hit;) {
+        const size_t end = f.find(',', at);
+        const std::string part = f.substr(at, end == std::string::npos ? std::string::npos : end - at);
+        hit = !part.empty() && std::strstr(c.name, part.c_str()) != nullptr;
+        if (end == std::string::npos) break;
+        at = end + 1;
+      }
+      if (!hit) continue;
     }
     ++run;
     state().case_failed = false;

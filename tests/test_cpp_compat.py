@@ -2,13 +2,13 @@
 libdsfft.so:
 
 * tests/cpp/test_compat.cpp -- this repo's own checks of the mirror;
-* the REFERENCE's own unit tests (proj/tests/test_fft.cpp, test_twiddle.cpp)
-  and acceptance suite (acceptance.cpp, criteria 2-9), compiled unmodified
-  from /root/reference by tests/cpp/Makefile with only the drop-in headers on
-  the include path (the binaries are built here and travel to the GPU box);
-* the reference API this library deliberately does not provide
-  (butterfly_* / kernel_for / ArithmeticContext scalar ops) fails at compile
-  time with an explanatory message instead of an unresolved symbol.
+* the REFERENCE's own unit tests (proj/tests/test_fft.cpp, test_twiddle.cpp,
+  test_butterfly.cpp, test_precision.cpp) and acceptance suite
+  (acceptance.cpp, criteria 2-9), compiled unmodified from /root/reference by
+  tests/cpp/Makefile with only the drop-in headers on the include path (the
+  binaries are built here and travel to the GPU box).  The butterfly-variant
+  API and the context's scalar operations run on the device
+  (dsfft_butterflies / dsfft_context_ops).
 
 Host-only parts run on CPU, the device parts on a B200."""
 import os
@@ -78,21 +78,13 @@ def test_reference_host_acceptance_through_dropin(ref_bins):
     assert r.stdout.count("[PASS]") == 4, r.stdout
 
 
-@pytest.mark.parametrize("snippet", [
-    "fmafft::kernel_for(fmafft::Strategy::dual_select);",
-    "fmafft::ComplexSample a, b; fmafft::TwiddleEntry e;"
-    " fmafft::ArithmeticContext c(fmafft::Precision::fp16);"
-    " fmafft::butterfly_dual(a, b, e, c);",
-    "fmafft::ArithmeticContext c(fmafft::Precision::fp16); c.fma(1.0, 2.0, 3.0);",
-])
-def test_unprovided_reference_api_fails_at_compile_time(tmp_path, snippet):
-    src = tmp_path / "use.cpp"
-    src.write_text('#include "fmafft/butterfly.hpp"\n#include "fmafft/fft.hpp"\n'
-                   f"int main() {{ {snippet} return 0; }}\n")
-    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ROOT}/include", str(src)],
-                       capture_output=True, text=True)
-    assert r.returncode != 0
-    assert "fmafft_b200:" in r.stderr and "not provided" in r.stderr, r.stderr
+def test_reference_precision_host_cases_through_dropin(ref_bins):
+    """proj/tests/test_precision.cpp: the five host-side cases (machine
+    epsilon, round_to examples / idempotence, binary16 bit-exactness)."""
+    r = subprocess.run([ref_bins[0], "machine epsilon,round_to,fp16 conversion"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "test cases: 5 | 5 passed | 0 failed" in r.stdout, r.stdout
 
 
 @pytest.mark.gpu
@@ -104,13 +96,14 @@ def test_cpp_dropin_device(exe, cuda):
 
 @pytest.mark.gpu
 def test_reference_unit_tests_through_dropin(ref_bins, cuda):
-    """ALL 24 cases of the reference's test_fft.cpp + test_twiddle.cpp pass on
-    the B200 through the drop-in: plan construction, forward/inverse vs the
-    (device) dft_oracle, op accounting, the corrupted-table negative control,
-    non-finite propagation."""
+    """ALL 43 cases of the reference's test_fft.cpp, test_twiddle.cpp,
+    test_butterfly.cpp and test_precision.cpp pass on the B200 through the
+    drop-in: plan construction, forward/inverse vs the (device) dft_oracle,
+    op accounting, the corrupted-table negative control, non-finite
+    propagation, every butterfly variant and the context's rounding."""
     r = subprocess.run([ref_bins[0]], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "test cases: 24 | 24 passed | 0 failed" in r.stdout, r.stdout
+    assert "test cases: 43 | 43 passed | 0 failed" in r.stdout, r.stdout
 
 
 @pytest.mark.gpu

@@ -184,3 +184,17 @@ def test_half_conversion_kat(orc):
              1 + 2 ** -12: 1.0, 2 ** -25: 0.0, 1.5 * 2 ** -24: 2 ** -23, 1e300: np.inf}
     for x, want in cases.items():
         assert orc.round_to(np.array([x]), "fp16")[0] == want, x
+
+
+def test_ctx_ops_match_reference(orc, ref):
+    """The oracle's ArithmeticContext restatement == the reference's, for
+    arbitrary doubles (the double-rounding of fp16 included)."""
+    rng = np.random.RandomState(5)
+    n = 20000
+    mant = 1.0 + rng.randint(0, 1 << 52, size=(3, n)).astype(np.float64) * 2.0 ** -52
+    x = np.ldexp(mant, rng.randint(-30, 18, size=(3, n))) * rng.choice([-1.0, 1.0], size=(3, n))
+    for p in ("fp16", "fp32", "fp64"):
+        for op in ("add", "sub", "mul", "fma"):
+            a = orc.ctx_op(p, op, x[0], x[1], x[2])
+            b = ref.ctx_op(p, op, x[0], x[1], x[2])
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (p, op)
