@@ -52,11 +52,11 @@ struct FusedParams {
   uint32_t scale;
 };
 
-template <int S1, class A, bool STANDARD, bool INVERSE, int MAXT, int SLAB>
-__global__ void __launch_bounds__(MAXT, 1)
+template <int S1, class A, bool STANDARD, bool INVERSE>
+__global__ void __launch_bounds__(512, 1)
     mp_fused_kernel(const __grid_constant__ CUtensorMap in_map,
                     const __grid_constant__ CUtensorMap mid_map, const FusedParams p) {
-  using Lay = MpLayout<S1, A, SLAB>;
+  using Lay = MpLayout<S1, A>;
   constexpr int L = Lay::L, T = Lay::T;
   constexpr int ROWS_BOX = L < 256 ? L : 256;
   constexpr int PAIR = A::kPair, EB = A::kSampleBytes, HALF = 32 * L * EB;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(MAXT, 1)
     if (!is_b) {
       uint32_t* done = p.done + tau * R + slot;
       const uint32_t* freed = p.freed + tau * R + slot;
-      mp_tile<S1, A, STANDARD, true, INVERSE, false, false, true, SLAB>(
+      mp_tile<S1, A, STANDARD, true, INVERSE, false, false, true>(
           buf_s, twA_base, nullptr, p.scale, 0, N, j, 0, true, g, warp, lane,
           [&] { return p.mid + (long long)(tau * R + slot) * N * kUnitScale; }, release,
           [&] {  // the slot's previous unit has been read by every member
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(MAXT, 1)
           if (has_next) issue(i + 1);
         }
       };
-      mp_tile<S1, A, STANDARD, false, false, INVERSE, true, false, SLAB>(
+      mp_tile<S1, A, STANDARD, false, false, INVERSE, true, false>(
           buf_s, twB_base, reinterpret_cast<const uint8_t*>(p.twB), p.scale, p.s, N, 0, j,
           b + 1 < p.nb, g, warp, lane, [&] { return p.out + b * N * EB; }, release_b, [] {});
     }
@@ -194,12 +194,12 @@ struct FusedShape {
   size_t smem = 0;
 };
 
-template <int S1, class A, int MAXT, int SLAB>
+template <int S1, class A>
 FusedShape fused_shape(int m, int sm_count, size_t smem_optin, long long units) {
-  using Lay = MpLayout<S1, A, SLAB>;
+  using Lay = MpLayout<S1, A>;
   FusedShape f;
   f.K = int((1LL << m) >> (5 + S1 + 5));  // column blocks per group (= 2^s / 32)
-  const int gmax = std::max(1, MAXT / Lay::T);
+  const int gmax = std::max(1, 512 / Lay::T);
   f.G = std::min(gmax, std::max(1, env_or("DSFFT_FUSED_GROUPS", gmax)));
   auto smem_for = [&](int G) {
     return size_t(Lay::tw_bytes(true)) + size_t(Lay::tw_bytes(false)) +
@@ -216,11 +216,11 @@ FusedShape fused_shape(int m, int sm_count, size_t smem_optin, long long units) 
   return f;
 }
 
-template <int S1, class A, bool STD, int MAXT, int SLAB>
+template <int S1, class A, bool STD>
 cudaError_t fused_launch_t(const CUtensorMap& in_map, const CUtensorMap& mid_map,
                            const FusedParams& p, const FusedShape& f, bool inverse,
                            cudaStream_t st) {
-  using Lay = MpLayout<S1, A, SLAB>;
+  using Lay = MpLayout<S1, A>;
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(f.smem));
@@ -237,16 +237,15 @@ cudaError_t fused_launch_t(const CUtensorMap& in_map, const CUtensorMap& mid_map
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, in_map, mid_map, p);
   };
-  return inverse ? go(mp_fused_kernel<S1, A, STD, true, MAXT, SLAB>)
-                 : go(mp_fused_kernel<S1, A, STD, false, MAXT, SLAB>);
+  return inverse ? go(mp_fused_kernel<S1, A, STD, true>) : go(mp_fused_kernel<S1, A, STD, false>);
 }
 
 template <class A>
 FusedShape fused_shape_a(int S1, int m, int sm, size_t optin, long long units) {
   switch (S1) {
-    case 2: return fused_shape<2, A, 512, -1>(m, sm, optin, units);
-    case 3: return fused_shape<3, A, 512, -1>(m, sm, optin, units);
-    case 4: return fused_shape<4, A, 512, -1>(m, sm, optin, units);
+    case 2: return fused_shape<2, A>(m, sm, optin, units);
+    case 3: return fused_shape<3, A>(m, sm, optin, units);
+    case 4: return fused_shape<4, A>(m, sm, optin, units);
   }
   return FusedShape{};
 }
@@ -256,9 +255,9 @@ cudaError_t fused_launch_a(int S1, const CUtensorMap& in_map, const CUtensorMap&
                            const FusedParams& p, const FusedShape& f, bool inverse,
                            cudaStream_t st) {
   switch (S1) {
-    case 2: return fused_launch_t<2, A, STD, 512, -1>(in_map, mid_map, p, f, inverse, st);
-    case 3: return fused_launch_t<3, A, STD, 512, -1>(in_map, mid_map, p, f, inverse, st);
-    case 4: return fused_launch_t<4, A, STD, 512, -1>(in_map, mid_map, p, f, inverse, st);
+    case 2: return fused_launch_t<2, A, STD>(in_map, mid_map, p, f, inverse, st);
+    case 3: return fused_launch_t<3, A, STD>(in_map, mid_map, p, f, inverse, st);
+    case 4: return fused_launch_t<4, A, STD>(in_map, mid_map, p, f, inverse, st);
   }
   return cudaErrorInvalidValue;
 }

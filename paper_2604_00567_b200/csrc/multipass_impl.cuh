@@ -28,7 +28,7 @@ __host__ __device__ constexpr int mp_block_records(int S1) {
   return 31 * 32 + (((1 << S1) - 1) << 10);
 }
 
-template <int S1, class A, int SLAB = -1>  // SLAB: -1 automatic, 0 stage-1 part only, 1 whole
+template <int S1, class A>
 struct MpLayout {
   static constexpr int s = 5 + S1, L = 1 << s, T = 32 << S1;
   static constexpr int VB = A::kWords * 4;
@@ -40,8 +40,7 @@ struct MpLayout {
   // 16-byte records up to S1 = 2); otherwise only the stage-1 part, and stage
   // 2 reads its records through L1 (ldg).  A 130 KB fp32 slab would leave room
   // for one 256-thread tile group per SM.
-  static constexpr bool kFullSlab =
-      SLAB >= 0 ? SLAB != 0 : S1 <= 3 && mp_block_records(S1) * A::kRecBytes <= 65536;
+  static constexpr bool kFullSlab = S1 <= 3 && mp_block_records(S1) * A::kRecBytes <= 65536;
   static constexpr int kSlabRecords = kFullSlab ? mp_block_records(S1) : 31 * 32;
   __host__ __device__ static constexpr int tw_bytes(bool first) {
     return ((first ? mp_first_records(S1) : kSlabRecords) * A::kRecBytes + 127) & ~127;
@@ -57,12 +56,12 @@ struct MpLayout {
 // pre_store() runs right before the scatter (the fused kernel waits there
 // until the scratch slot it writes is free).
 template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST,
-          bool BOUT, int SLAB = -1, class Out, class Release, class PreStore>
+          bool BOUT, class Out, class Release, class PreStore>
 __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const uint8_t* tw_g,
                                         uint32_t scale, int P, long long N, long long q, int rb,
                                         bool second, int g, int warp, int lane, Out&& out,
                                         Release&& release, PreStore&& pre_store) {
-  using Lay = MpLayout<S1, A, SLAB>;
+  using Lay = MpLayout<S1, A>;
   constexpr int L = Lay::L, T = Lay::T, NG2 = 32 >> S1, VB = Lay::VB;
   constexpr int STRIDE = L + 1;  // padded exchange column (values)
   constexpr int RB = A::kRecBytes;
