@@ -796,6 +796,8 @@ int dsfft_dft_device(const void* d_in, void* d_out, size_t n, size_t batch, int 
   if (!d_in || !d_out) return fail(DSFFT_ERR_INVALID, "null buffer");
   if (n < 1 || n > (size_t(1) << 24)) return fail(DSFFT_ERR_INVALID, "dft_oracle: n out of range");
   if (d_in == d_out) return fail(DSFFT_ERR_INVALID, "dft_oracle is out of place");
+  if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+    return fail(DSFFT_ERR_INVALID, "device buffers must be 16-byte aligned");
   if (batch == 0) return DSFFT_OK;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
