@@ -64,10 +64,10 @@ struct MpParams {
 // and group g takes transforms b0+g, b0+g+G, ... of the unit with its own TMA
 // ring.  Register budget: one-word values ~80, two-word ~128.
 template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST,
-          bool BOUT>
+          bool BOUT, int CW>
 __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     mp_kernel(const __grid_constant__ CUtensorMap in_map, const MpParams p) {
-  using Lay = MpLayout<S1, A>;
+  using Lay = MpLayout<S1, A, CW>;
   constexpr int L = Lay::L, T = Lay::T;
   constexpr int ROWS_BOX = L < 256 ? L : 256;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -104,31 +104,33 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   // b+1 past the batch is zero-filled by TMA and never stored)
   constexpr int PAIR = A::kPair;
   constexpr int EB = A::kSampleBytes;           // bytes of one complex in memory
-  constexpr int HALF = 32 * L * EB;             // one transform's tile
+  constexpr int HALF = CW * L * EB;             // one transform's tile
   // fp16 pairs keep intermediates pair-packed: 8-byte values (re0,re1),(im0,im1)
   // of transforms (b, b+1) at pair index b/2 -- no unpack/repack between groups
   constexpr bool PIN = PAIR == 2 && !FIRST;
-  auto issue_load = [&](long long q, int rb, int b, int slot) {
+  // hf: which CW-wide part of a later group's 32-column block (CW = 16: 0, 1)
+  auto issue_load = [&](long long q, int rb, int hf, int b, int slot) {
     uint8_t* dst = bufs + size_t(slot) * Lay::kBufBytes;
     ptx::mbar_arrive_expect_tx(&bars[slot], Lay::kTileBytes);
 #pragma unroll
     for (int h = 0; h < (PIN ? 1 : PAIR); ++h)
 #pragma unroll
       for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
-        uint8_t* d = dst + h * HALF + size_t(r0) * 32 * (PIN ? 8 : EB);
+        uint8_t* d = dst + h * HALF + size_t(r0) * CW * (PIN ? 8 : EB);
         const int bb = PIN ? b / 2 : int(b + h + p.b_off);
         if constexpr (FIRST)
-          ptx::tma_load_3d(d, &in_map, int(q * 32), r0, bb, &bars[slot], pol);
+          ptx::tma_load_3d(d, &in_map, int(q * CW), r0, bb, &bars[slot], pol);
         else if constexpr (LAST)  // blocked intermediate {r_l, c, rb, b}
-          ptx::tma_load_4d(d, &in_map, 0, r0, rb, bb, &bars[slot], pol);
+          ptx::tma_load_4d(d, &in_map, hf * CW, r0, rb, bb, &bars[slot], pol);
         else
-          ptx::tma_load_4d(d, &in_map, rb * 32, int(q), r0, bb, &bars[slot], pol);
+          ptx::tma_load_4d(d, &in_map, rb * 32 + hf * CW, int(q), r0, bb, &bars[slot], pol);
       }
   };
-  auto tile = [&](long long q, int rb, int b, bool second, uint32_t buf, auto&& release) {
-    mp_tile<S1, A, STANDARD, FIRST, CONJ_IN, SCALE_OUT, LAST, BOUT>(
-        buf, tw_base, reinterpret_cast<const uint8_t*>(p.tw), p.scale, P, N, q, rb, second, g,
-        warp, lane, [&] { return p.out + b * N * EB; },  // == pair b/2 * N * 8 for packed pairs
+  auto tile = [&](long long q, int rb, int hf, int b, bool second, uint32_t buf,
+                  auto&& release) {
+    mp_tile<S1, A, STANDARD, FIRST, CONJ_IN, SCALE_OUT, LAST, BOUT, CW>(
+        buf, tw_base, reinterpret_cast<const uint8_t*>(p.tw), p.scale, P, N, q, rb, hf * CW,
+        second, g, warp, lane, [&] { return p.out + b * N * EB; },  // pair b/2 * N * 8 if packed
         release, [] {});
   };
 
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     // Tiles in transform-major order (column block fastest): a CTA walks all
     // column blocks of one transform (pair) before the next, so the rows it
     // reads share DRAM pages; the twiddles are column-independent.
-    const long long nblk = (N >> Lay::s) >> 5;
+    const long long nblk = (N >> Lay::s) / CW;
     const long long total = nblk * ((p.nb + PAIR - 1) / PAIR);
     const long long per = (total + gridDim.x - 1) / gridDim.x;
     const long long t_begin = blockIdx.x * per;
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
     auto load_tile = [&](int i) {
       const long long idx = first_idx + (long long)G * i;
       const long long pr = idx / nblk;
-      issue_load(idx - pr * nblk, 0, int(pr * PAIR), i % S);
+      issue_load(idx - pr * nblk, 0, 0, int(pr * PAIR), i % S);
     };
     if (leader)
       for (int i = 0; i < S && i < k; ++i) load_tile(i);
@@ -156,23 +158,26 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
       const int b = int(pr * PAIR);
       const int slot = i % S;
       ptx::mbar_wait(&bars[slot], uint32_t((i / S) & 1));
-      tile(idx - pr * nblk, 0, b, PAIR == 2 && b + 1 < nb,
+      tile(idx - pr * nblk, 0, 0, b, PAIR == 2 && b + 1 < nb,
            ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
              if (leader && i + S < k) load_tile(i + S);
            });
     }
   } else {
-    // units of PAIR transforms, column block outer: tile u -> (tt, pair v)
+    // units of PAIR transforms, column block outer: tile u -> (tt, pair v,
+    // part hf of the block when CW = 16)
+    constexpr int HPB = 32 / CW;
     const long long nbu = (p.nb + PAIR - 1) / PAIR;
-    const long long total = ((N >> Lay::s) >> 5) * nbu;
+    const long long per_blk = nbu * HPB;
+    const long long total = ((N >> Lay::s) >> 5) * per_blk;
     const long long per = (total + gridDim.x - 1) / gridDim.x;
     const long long t_begin = blockIdx.x * per;
     const long long t_end = t_begin + per < total ? t_begin + per : total;
     long long it = 0;  // this group's running tile count (ring slot / phase)
     for (long long u0 = t_begin; u0 < t_end;) {
-      const long long tt = u0 / nbu;  // column block of this unit
-      const int v0 = int(u0 - tt * nbu);
-      const long long u1 = (tt + 1) * nbu < t_end ? (tt + 1) * nbu : t_end;
+      const long long tt = u0 / per_blk;  // column block of this unit
+      const long long w0 = u0 - tt * per_blk;
+      const long long u1 = (tt + 1) * per_blk < t_end ? (tt + 1) * per_blk : t_end;
       const int units = int(u1 - u0);
       u0 = u1;
       const long long q = tt / rblocks;
@@ -186,16 +191,18 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
         __syncthreads();
       }
       const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
+      auto item_b = [&](int i) { return int(PAIR * ((w0 + g + (long long)G * i) / HPB)); };
+      auto item_hf = [&](int i) { return int((w0 + g + (long long)G * i) % HPB); };
       if (leader)
         for (int i = 0; i < S && i < k; ++i)
-          issue_load(q, rb, PAIR * (v0 + g + G * i), int((it + i) % S));
+          issue_load(q, rb, item_hf(i), item_b(i), int((it + i) % S));
       for (int i = 0; i < k; ++i) {
-        const int b = PAIR * (v0 + g + G * i);
+        const int b = item_b(i);
         const int slot = int((it + i) % S);
         ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
-        tile(q, rb, b, PAIR == 2 && b + 1 < nb,
+        tile(q, rb, item_hf(i), b, PAIR == 2 && b + 1 < nb,
              ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
-               if (leader && i + S < k) issue_load(q, rb, b + PAIR * G * S, slot);
+               if (leader && i + S < k) issue_load(q, rb, item_hf(i + S), item_b(i + S), slot);
              });
       }
       it += k;
@@ -234,7 +241,7 @@ std::vector<int> split_passes(int m, int max_s) {
     bool ok = true;
     for (const char* c = env; *c;) {
       const int s = std::atoi(c);
-      ok = ok && s >= 6 && s <= 9;
+      ok = ok && s >= 6 && s <= max_s;
       v.push_back(s);
       sum += s;
       while (*c && *c != ',') ++c;
@@ -243,11 +250,12 @@ std::vector<int> split_passes(int m, int max_s) {
     if (ok && sum == m && v.size() >= 2) return v;
   }
   // 2 groups up to m = 2*max_s, 3 beyond; every group 6..max_s passes.
-  // max_s = 9 for every value width: at 8-byte values (fp32, fp16 pairs) an
-  // s = 9 tile is 128 KiB, so mp_launch_t falls back to one 1-deep tile group
-  // per CTA there (m = 17, 18); the 3-group split that max_s = 8 would force
-  // instead measured within +-3% (profiles/r01_sweep.md) and
-  // costs a third HBM round trip.
+  // max_s = 10 for 8-byte values (fp32, fp16 pairs): s = 10 runs 16-column x
+  // 1024-row tiles (128 KiB, one 512-thread group per CTA), so N = 2^19 and
+  // 2^20 take two HBM round trips; s = 9 tiles (32 x 512, 128 KiB) likewise
+  // fall back to one 1-deep group per CTA (m = 17, 18), which measured within
+  // +-3% of the 3-group splits that smaller tiles would force.  One-word fp16
+  // values keep max_s = 9.
   if (m <= 2 * max_s) {
     const int a = (m + 1) / 2;
     return {a, m - a};
@@ -267,7 +275,7 @@ int env_or(const char* name, int dflt) {
 
 // Input map of a pass group over `batch` transforms starting at `base`.
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
-                long long batch) {
+                long long batch, int box_cols) {
   EncodeFn enc = encode_fn();
   if (!enc) return -1;
   const CUtensorMapDataType dt =
@@ -279,14 +287,14 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
   if (P == 0) {  // {q (N/2^s), c (2^s), b}
     cuuint64_t dims[3] = {N >> s, cuuint64_t(1) << s, cuuint64_t(batch)};
     cuuint64_t strides[2] = {(N >> s) * vb, N * vb};
-    cuuint32_t box[3] = {32, rows_box, 1};
+    cuuint32_t box[3] = {cuuint32_t(box_cols), rows_box, 1};
     r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (P + s == m) {  // last group: blocked intermediate {r_l, c, rb, b}
     cuuint64_t dims[4] = {32, cuuint64_t(1) << s, N >> (s + 5), cuuint64_t(batch)};
     cuuint64_t strides[3] = {32 * cuuint64_t(vb), (cuuint64_t(32) << s) * vb, N * vb};
-    cuuint32_t box[4] = {32, rows_box, 1, 1};
+    cuuint32_t box[4] = {cuuint32_t(box_cols), rows_box, 1, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -294,7 +302,7 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
     cuuint64_t dims[4] = {cuuint64_t(1) << P, N >> (P + s), cuuint64_t(1) << s,
                           cuuint64_t(batch)};
     cuuint64_t strides[3] = {(cuuint64_t(1) << P) * vb, (N >> s) * vb, N * vb};
-    cuuint32_t box[4] = {32, 1, rows_box, 1};
+    cuuint32_t box[4] = {cuuint32_t(box_cols), 1, rows_box, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -305,20 +313,21 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
 
 namespace {
 
-template <int S1, class A, bool STD>
+template <int S1, class A, bool STD, int CW>
 cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, bool conj_in,
                         bool scale_out, bool last, bool bout, int sm_count, size_t smem_optin,
                         cudaStream_t st) {
-  using Lay = MpLayout<S1, A>;
+  using Lay = MpLayout<S1, A, CW>;
   MpParams q = p;
   // ring depth S and tile groups per CTA G (later groups share one
-  // column-block slab between their G groups; <= 512 threads).  Default: two
-  // independent groups, giving up ring depth before groups when shared memory
-  // is short -- two 1-deep groups beat one 2-deep group by 0-3% (B200 sweep).
+  // column-block slab between their G groups; <= 512 threads).  Default: as
+  // many independent groups as 512 threads hold (two 32-column groups, four
+  // 16-column ones), giving up ring depth before groups when shared memory is
+  // short -- two 1-deep groups beat one 2-deep group by 0-3% (B200 sweep).
   const char* es = std::getenv("DSFFT_MP_STAGES");
   const char* eg = std::getenv("DSFFT_MP_GROUPS");
   int stages = es && *es ? std::max(1, std::atoi(es)) : 2;
-  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : 2;
+  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : 512 / Lay::T;
   groups = std::min(groups, std::max(1, 512 / Lay::T));
   while (stages > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --stages;
   while (groups > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --groups;
@@ -340,27 +349,42 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
   };
   // the group before the last writes the blocked intermediate (bout)
   if (first && bout)  // never last: every split has >= 2 groups
-    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, true>)
-                   : go(mp_kernel<S1, A, STD, true, false, false, false, true>);
+    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, true, CW>)
+                   : go(mp_kernel<S1, A, STD, true, false, false, false, true, CW>);
   if (first)
-    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, false>)
-                   : go(mp_kernel<S1, A, STD, true, false, false, false, false>);
+    return conj_in ? go(mp_kernel<S1, A, STD, true, true, false, false, false, CW>)
+                   : go(mp_kernel<S1, A, STD, true, false, false, false, false, CW>);
   if (last)
-    return scale_out ? go(mp_kernel<S1, A, STD, false, false, true, true, false>)
-                     : go(mp_kernel<S1, A, STD, false, false, false, true, false>);
-  return go(mp_kernel<S1, A, STD, false, false, false, false, true>);  // middle of 3
+    return scale_out ? go(mp_kernel<S1, A, STD, false, false, true, true, false, CW>)
+                     : go(mp_kernel<S1, A, STD, false, false, false, true, false, CW>);
+  return go(mp_kernel<S1, A, STD, false, false, false, false, true, CW>);  // middle of 3
 }
 
+// cw: columns per tile; 16-column tiles exist for two-word values (fp32, fp16
+// pairs: 128-byte rows) at s >= 7
 template <class A, bool STD>
-cudaError_t mp_launch_a(int S1, const CUtensorMap& map, const MpParams& p, bool first,
+cudaError_t mp_launch_a(int S1, int cw, const CUtensorMap& map, const MpParams& p, bool first,
                         bool conj_in, bool scale_out, bool last, bool bout, int sm_count,
                         size_t optin, cudaStream_t st) {
-  switch (S1) {
-    case 1: return mp_launch_t<1, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
-    case 2: return mp_launch_t<2, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
-    case 3: return mp_launch_t<3, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
-    case 4: return mp_launch_t<4, A, STD>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st);
+#define DSFFT_MP_GO(S, C) \
+  mp_launch_t<S, A, STD, C>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st)
+  if constexpr (A::kWords == 2) {
+    if (cw == 16) {
+      switch (S1) {
+        case 2: return DSFFT_MP_GO(2, 16);
+        case 3: return DSFFT_MP_GO(3, 16);
+        case 4: return DSFFT_MP_GO(4, 16);
+        case 5: return DSFFT_MP_GO(5, 16);  // s = 10: 16 x 1024 tiles (128 KB)
+      }
+    }
   }
+  switch (S1) {
+    case 1: return DSFFT_MP_GO(1, 32);
+    case 2: return DSFFT_MP_GO(2, 32);
+    case 3: return DSFFT_MP_GO(3, 32);
+    case 4: return DSFFT_MP_GO(4, 32);
+  }
+#undef DSFFT_MP_GO
   return cudaErrorInvalidValue;
 }
 
@@ -392,8 +416,11 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   mp->fused = !f16c && m % 2 == 0 && m >= 14 && m <= 18 && env_or("DSFFT_MP_FUSED", 0) != 0;
   auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
   int P = 0;
+  // two-word values (fp32, fp16 pairs) take s = 10 groups as 16-column tiles,
+  // so N = 2^19, 2^20 need two HBM round trips instead of three
+  const int max_s = f16c ? 9 : 10;
   const std::vector<int> split =
-      mp->fused ? std::vector<int>{m / 2, m / 2} : split_passes(m, 9);
+      mp->fused ? std::vector<int>{m / 2, m / 2} : split_passes(m, max_s);
   for (int s : split) {
     MpGroup g;
     g.P = P;
@@ -458,6 +485,14 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
                       uint32_t scale, cudaStream_t stream, uint64_t* launches) {
   const int vb = int(sample_bytes(mp.precision));
   const size_t tb = (size_t(1) << mp.m) * vb;
+  // columns per tile: 16 for s = 10 (a 32 x 1024 tile of 8-byte values would
+  // not fit shared memory), or everywhere from s = 7 with DSFFT_MP_CW=16
+  auto tile_cols = [&](int s) {
+    return s == 10 || (env_or("DSFFT_MP_CW", 32) == 16 &&
+                       !(mp.precision == kFp16 && !mp.f16_pairs) && s >= 7)
+               ? 16
+               : 32;
+  };
   const bool f16 = mp.precision == kFp16;
   const bool std_ = mp.strategy == kStandard;
   const int ng = int(mp.groups.size());
@@ -492,7 +527,8 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
     // elements, one map "batch" entry per transform pair
     const bool packed = i > 0 && f16 && mp.f16_pairs;
     const int rc = make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s,
-                               packed ? 8 : vb, packed ? (nb + 1) / 2 : nb);
+                               packed ? 8 : vb, packed ? (nb + 1) / 2 : nb,
+                               tile_cols(mp.groups[i].s));
     if (rc != 0) {
       g_mp_err = "multipass: cuTensorMapEncodeTiled failed (CUresult " + std::to_string(rc) +
                  ", group " + std::to_string(i) + ", base " +
@@ -512,23 +548,23 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       p.P = g.P;
       p.nb = (long long)nb;
       p.b_off = i == 0 ? (long long)b0 : 0;
-      p.tiles = (((1LL << mp.m) >> g.s) / 32) * (long long)nb;
+      p.tiles = (((1LL << mp.m) >> g.s) / tile_cols(g.s)) * (long long)nb;
       p.scale = scale;
       const bool first = i == 0, last = i == ng - 1;
-      const int S1 = g.s - 5;
+      const int S1 = g.s - 5, cw = tile_cols(g.s);
       const bool ci = first && inverse, so = last && inverse, bo = i == ng - 2;
       const int sm = mp.sm_count;
       const size_t oi = mp.smem_optin;
       cudaError_t e;
       if (f16 && mp.f16_pairs)
-        e = std_ ? mp_launch_a<ArithF16P, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
-                 : mp_launch_a<ArithF16P, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF16P, true>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF16P, false>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       else if (f16)
-        e = std_ ? mp_launch_a<ArithF16C, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
-                 : mp_launch_a<ArithF16C, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF16C, true>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF16C, false>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       else
-        e = std_ ? mp_launch_a<ArithF32, true>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
-                 : mp_launch_a<ArithF32, false>(S1, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
+        e = std_ ? mp_launch_a<ArithF32, true>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream)
+                 : mp_launch_a<ArithF32, false>(S1, cw, maps[i], p, first, ci, so, last, bo, sm, oi, stream);
       if (e != cudaSuccess) {
         g_mp_err = std::string("mp_kernel launch: ") + cudaGetErrorString(e);
         return 1;

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(512, 1)
       uint32_t* done = p.done + tau * R + slot;
       const uint32_t* freed = p.freed + tau * R + slot;
       mp_tile<S1, A, STANDARD, true, INVERSE, false, false, true>(
-          buf_s, twA_base, nullptr, p.scale, 0, N, j, 0, true, g, warp, lane,
+          buf_s, twA_base, nullptr, p.scale, 0, N, j, 0, 0, true, g, warp, lane,
           [&] { return p.mid + (long long)(tau * R + slot) * N * kUnitScale; }, release,
           [&] {  // the slot's previous unit has been read by every member
             ptx::wait_at_least(freed, uint32_t(K) * uint32_t(v / R));
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(512, 1)
         }
       };
       mp_tile<S1, A, STANDARD, false, false, INVERSE, true, false>(
-          buf_s, twB_base, reinterpret_cast<const uint8_t*>(p.twB), p.scale, p.s, N, 0, j,
+          buf_s, twB_base, reinterpret_cast<const uint8_t*>(p.twB), p.scale, p.s, N, 0, j, 0,
           b + 1 < p.nb, g, warp, lane, [&] { return p.out + b * N * EB; }, release_b, [] {});
     }
   }

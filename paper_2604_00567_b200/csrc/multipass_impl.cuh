@@ -28,12 +28,14 @@ __host__ __device__ constexpr int mp_block_records(int S1) {
   return 31 * 32 + (((1 << S1) - 1) << 10);
 }
 
-template <int S1, class A>
+// CW: columns per tile (32, or 16 -- narrower tiles, twice the tile groups
+// per SM, same full-sector rows for 8-byte values).
+template <int S1, class A, int CW = 32>
 struct MpLayout {
-  static constexpr int s = 5 + S1, L = 1 << s, T = 32 << S1;
+  static constexpr int s = 5 + S1, L = 1 << s, T = CW << S1;
   static constexpr int VB = A::kWords * 4;
-  static constexpr int kBufBytes = 32 * (L + 1) * VB;  // padded exchange >= TMA tile
-  static constexpr int kTileBytes = 32 * L * VB;
+  static constexpr int kBufBytes = CW * (L + 1) * VB;  // padded exchange >= TMA tile
+  static constexpr int kTileBytes = CW * L * VB;
   // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned.
   // Later groups keep their column block's whole twiddle slab in smem (stage 1
   // and 2) when it is at most 64 KB (8-byte fp16 pair records up to S1 = 3,
@@ -55,31 +57,41 @@ struct MpLayout {
 // c.buf.  release() hands the slot back to TMA after its last smem read;
 // pre_store() runs right before the scatter (the fused kernel waits there
 // until the scratch slot it writes is free).
+//
+// Threads: `sub` = warp * (32 / CW) + lane / CW takes rows sub + 2^S1 c of
+// column `col` = lane % CW in stage 1.  Stage 2 groups (column, r_l): first
+// group -- lanes walk r_l (column-contiguous output), columns warp + NW j;
+// later groups -- lanes walk columns, r_l = sub + 2^S1 j.  col_off places a
+// 16-column tile inside its 32-column block (twiddle slab, output columns).
 template <int S1, class A, bool STANDARD, bool FIRST, bool CONJ_IN, bool SCALE_OUT, bool LAST,
-          bool BOUT, class Out, class Release, class PreStore>
+          bool BOUT, int CW = 32, class Out, class Release, class PreStore>
 __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const uint8_t* tw_g,
                                         uint32_t scale, int P, long long N, long long q, int rb,
-                                        bool second, int g, int warp, int lane, Out&& out,
-                                        Release&& release, PreStore&& pre_store) {
-  using Lay = MpLayout<S1, A>;
+                                        int col_off, bool second, int g, int warp, int lane,
+                                        Out&& out, Release&& release, PreStore&& pre_store) {
+  using Lay = MpLayout<S1, A, CW>;
   constexpr int L = Lay::L, T = Lay::T, NG2 = 32 >> S1, VB = Lay::VB;
+  constexpr int NW = T / 32;           // warps per group
+  constexpr int NSUB = 32 / CW;        // row phases per warp
+  const int sub = warp * NSUB + (NSUB == 1 ? 0 : lane / CW);
+  const int col = lane % CW, col32 = col_off + col;
   constexpr int STRIDE = L + 1;  // padded exchange column (values)
   constexpr int RB = A::kRecBytes;
   constexpr int PAIR = A::kPair;
   constexpr int EB = A::kSampleBytes;  // bytes of one complex in memory
-  constexpr int HALF = 32 * L * EB;    // one transform's tile
+  constexpr int HALF = CW * L * EB;    // one transform's tile
   constexpr bool PIN = PAIR == 2 && !FIRST, POUT = PAIR == 2 && !LAST;
   constexpr int OEB = POUT ? 8 : EB;   // bytes per stored output element
   auto group_sync = [&]() {
     if (T == 32) __syncwarp(); else ptx::named_bar_sync(1 + g, T);
   };
   uint32_t re[32], im[32];
-  // ---- stage 1: rows warp + c*2^S1 of column `lane` (tile is [row][32]) --
+  // ---- stage 1: rows sub + c*2^S1 of column `col` (tile is [row][CW]) ----
 #pragma unroll
   for (int cc = 0; cc < 32; ++cc) {
-    [[maybe_unused]] const uint32_t a = buf + (((warp + (cc << S1)) << 5) + lane) * VB;
+    [[maybe_unused]] const uint32_t a = buf + ((sub + (cc << S1)) * CW + col) * VB;
     if constexpr (PAIR == 2 && !PIN) {  // (re0,re1), (im0,im1) from the two halves
-      const uint32_t e = buf + (((warp + (cc << S1)) << 5) + lane) * EB;
+      const uint32_t e = buf + ((sub + (cc << S1)) * CW + col) * EB;
       const uint32_t lo = ptx::lds32(e), hi = ptx::lds32(e + HALF);
       re[cc] = __byte_perm(lo, hi, 0x5410);
       im[cc] = __byte_perm(lo, hi, 0x7632);
@@ -99,7 +111,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
     for (int rl = 0; rl < (1 << pl); ++rl) {
       const int slot1 = (1 << pl) - 1 + rl;
       const uint4 tw = FIRST ? load_rec<A>(tw_base + slot1 * RB)
-                             : load_rec<A>(tw_base + (slot1 * 32 + lane) * RB);
+                             : load_rec<A>(tw_base + (slot1 * 32 + col32) * RB);
 #pragma unroll
       for (int qq = 0; qq < (16 >> pl); ++qq) {
         const int jl = (qq << pl) | rl;
@@ -118,7 +130,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   group_sync();  // every stage-1 read of the TMA tile is done
 #pragma unroll
   for (int cc = 0; cc < 32; ++cc) {
-    const uint32_t a = buf + (lane * STRIDE + warp * 32 + cc) * VB;
+    const uint32_t a = buf + (col * STRIDE + sub * 32 + cc) * VB;
     if constexpr (A::kWords == 1) ptx::sts32(a, re[cc]); else ptx::sts64(a, re[cc], im[cc]);
   }
   group_sync();
@@ -126,11 +138,11 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   // column output), later groups lanes walk columns (contiguous rows)
 #pragma unroll
   for (int j = 0; j < NG2; ++j) {
-    const int col = FIRST ? warp + (j << S1) : lane;
-    const int rl_ = FIRST ? lane : warp + (j << S1);
+    const int col2 = FIRST ? warp + NW * j : col;
+    const int rl_ = FIRST ? lane : sub + (j << S1);
 #pragma unroll
     for (int cc = 0; cc < (1 << S1); ++cc) {
-      const uint32_t a = buf + (col * STRIDE + rl_ + 32 * cc) * VB;
+      const uint32_t a = buf + (col2 * STRIDE + rl_ + 32 * cc) * VB;
       const int v = (j << S1) + cc;
       if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
     }
@@ -142,7 +154,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   // ---- stage 2 ----------------------------------------------------------
   [[maybe_unused]] const uint8_t* tw2 =
       FIRST ? nullptr
-            : tw_g + ((long long)rb * mp_block_records(S1) + 31 * 32 + warp * 32 + lane) * RB;
+            : tw_g + ((long long)rb * mp_block_records(S1) + 31 * 32 + sub * 32 + col32) * RB;
 #pragma unroll
   for (int pl = 0; pl < S1; ++pl) {
     uint32_t nre[32], nim[32];
@@ -154,10 +166,10 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
         uint4 tw;
         if constexpr (FIRST)
           tw = load_rec<A>(tw_base + (31 + (slot2 << 5) + lane) * RB);
-        else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + lane
-          tw = load_rec<A>(tw_base + (31 * 32 + (warp << 5) + lane +
+        else if constexpr (Lay::kFullSlab)  // record (slot2*32 + r_l)*32 + column
+          tw = load_rec<A>(tw_base + (31 * 32 + (sub << 5) + col32 +
                                       (((slot2 << 5) + (j << S1)) << 5)) * RB);
-        else  // r_l = warp + 2^S1 j
+        else  // r_l = sub + 2^S1 j
           tw = ldg_rec<A>(tw2 + ((slot2 << 5) + (j << S1)) * 32 * RB);
 #pragma unroll
         for (int qq = 0; qq < ((1 << (S1 - 1)) >> pl); ++qq) {
@@ -184,22 +196,22 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   uint8_t* gout = out();  // this transform (pair) in the group's output
   [[maybe_unused]] const long long S3 = N >> (P + Lay::s);  // rows of the last group (BOUT)
   uint8_t* base;
-  long long jstride, cstride;  // bytes between values j<<S1 and rows c'
-  if constexpr (FIRST && BOUT) {  // r' = lane + 32 c, c-index = column
-    base = gout + ((q * 32 + warp) * 32 + lane) * OEB;
-    jstride = 32LL * OEB;
+  long long jstride, cstride;  // bytes between groups j and rows c'
+  if constexpr (FIRST && BOUT) {  // r' = lane + 32 c, c-index = column q CW + warp + NW j
+    base = gout + ((q * CW + warp) * 32 + lane) * OEB;
+    jstride = 32LL * NW * OEB;
     cstride = S3 * 32 * OEB;
-  } else if constexpr (FIRST) {  // column-contiguous: ((32 q + col) L + r_l + 32 c')
-    base = gout + ((q * 32 + warp) * L + lane) * OEB;
-    jstride = (long long)L * OEB;
+  } else if constexpr (FIRST) {  // column-contiguous: ((q CW + col) L + r_l + 32 c')
+    base = gout + ((q * CW + warp) * L + lane) * OEB;
+    jstride = (long long)L * NW * OEB;
     cstride = 32 * OEB;
-  } else if constexpr (BOUT) {  // r' = rb*32 + lane + 2^P (warp + 2^S1 j + 32 c)
-    base = gout + (((rb + ((long long)warp << (P - 5))) * S3 + q) * 32 + lane) * OEB;
-    jstride = (S3 * 32 * OEB) << (P - 5);
+  } else if constexpr (BOUT) {  // r' = rb*32 + col32 + 2^P (sub + 2^S1 j + 32 c)
+    base = gout + (((rb + ((long long)sub << (P - 5))) * S3 + q) * 32 + col32) * OEB;
+    jstride = ((S3 * 32 * OEB) << (P - 5)) << S1;
     cstride = ((S3 * 32 * OEB) << (P - 5)) * 32;
   } else {
-    base = gout + ((q << (P + Lay::s)) + rb * 32 + lane + ((long long)warp << P)) * OEB;
-    jstride = (long long)OEB << P;
+    base = gout + ((q << (P + Lay::s)) + rb * 32 + col32 + ((long long)sub << P)) * OEB;
+    jstride = ((long long)OEB << P) << S1;
     cstride = ((long long)OEB << P) * 32;
   }
 #pragma unroll
@@ -217,7 +229,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
           xi = A::mul(A::neg(xi), scale);
         }
       }
-      uint8_t* dst = base + (j << S1) * jstride + cc * cstride;
+      uint8_t* dst = base + j * jstride + cc * cstride;
       if constexpr (POUT) {  // pair-packed intermediate
         __stcg(reinterpret_cast<uint2*>(dst), make_uint2(xr, xi));
       } else if constexpr (PAIR == 2) {  // unpack to transforms b and b+1
@@ -266,7 +278,7 @@ void set_mp_error(const std::string& msg);
 int env_or(const char* name, int dflt);
 // TMA map over `batch` transforms at `base` for pass group [P, P+s) (see multipass.cu)
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
-                long long batch);
+                long long batch, int box_cols = 32);
 // one-launch execution of an eligible plan (multipass_fused.cu)
 int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, size_t batch,
                   uint32_t scale, cudaStream_t stream, uint64_t* launches);
