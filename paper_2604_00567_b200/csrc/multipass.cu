@@ -232,7 +232,7 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-std::vector<int> split_passes(int m, int max_s) {
+std::vector<int> split_passes(int m, int max_s, bool fp32) {
   // DSFFT_MP_SPLIT="a,b[,c]" overrides (tuning; ignored unless every group is
   // 6..9 passes and they sum to m)
   if (const char* env = std::getenv("DSFFT_MP_SPLIT")) {
@@ -257,7 +257,16 @@ std::vector<int> split_passes(int m, int max_s) {
   // +-3% of the 3-group splits that smaller tiles would force.  One-word fp16
   // values keep max_s = 9.
   if (m <= 2 * max_s) {
-    const int a = (m + 1) / 2;
+    if (max_s < 10) {  // one-word fp16 values
+      const int a = (m + 1) / 2;
+      return {a, m - a};
+    }
+    // 8-byte values: the larger group last (the first group reads the user's
+    // rows, the last the blocked intermediate), except where the B200 sweep
+    // (profiles/r02_fused_multipass.md, "pass-group splits") measured the
+    // other way for fp32: m = 18 as 8 + 10 (+9% over 9 + 9) and m = 19 as
+    // 10 + 9 (+15% over 9 + 10)
+    const int a = fp32 && m == 18 ? 8 : fp32 && m == 19 ? 10 : m / 2;
     return {a, m - a};
   }
   const int a = (m + 2) / 3, b = (m - a + 1) / 2;
@@ -420,7 +429,7 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   // so N = 2^19, 2^20 need two HBM round trips instead of three
   const int max_s = f16c ? 9 : 10;
   const std::vector<int> split =
-      mp->fused ? std::vector<int>{m / 2, m / 2} : split_passes(m, max_s);
+      mp->fused ? std::vector<int>{m / 2, m / 2} : split_passes(m, max_s, precision == kFp32);
   for (int s : split) {
     MpGroup g;
     g.P = P;
