@@ -106,9 +106,13 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def kernel_name(n: int) -> str:
-    """The dominant kernel of the workload (single kernel N <= 8192)."""
-    return "fft_small_kernel" if n <= 8192 else "mp_kernel"
+def kernel_name(n: int, launches_per_step: int) -> str:
+    """The dominant kernel of the workload: the single kernel for N <= 8192;
+    above, the fused one-launch kernel when the library chose it (one launch
+    per step), else the pass-group kernel."""
+    if n <= 8192:
+        return "fft_small_kernel"
+    return "mp_fused_kernel" if launches_per_step == 1 else "mp_kernel"
 
 
 def load_traffic(args, batch):
@@ -455,7 +459,7 @@ def main():
             "hbm_gbs": 2.0 * n * sbytes * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_kind": peak_kind, "kernel": kernel_name(n),
+                         "peak_kind": peak_kind, "kernel": kernel_name(n, launches_per_step),
                          "traffic_from": traffic_kernel,
                          "launches_per_step": launches_per_step,
                          "algorithmic_bytes_per_step": algo_bytes,

@@ -418,11 +418,15 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   const bool f16c = precision == kFp16 && !mp->f16_pairs;
   // one launch, L2-resident intermediate (multipass_fused.cu): m = 2s with s
   // in 7..9 (N = 2^14, 2^16, 2^18), two-word values (fp32, fp16 transform
-  // pairs).  Opt-in (DSFFT_MP_FUSED=1): it moves 1.01x the algorithmic DRAM
-  // bytes (vs 2x) and stays under the board power cap, but with two
-  // 256-thread tile groups per SM (128 registers, ~200 KB smem) it is bound by
-  // SM latency, and measures 0.85-1.12x the two-launch path (profiles/).
-  mp->fused = !f16c && m % 2 == 0 && m >= 14 && m <= 18 && env_or("DSFFT_MP_FUSED", 0) != 0;
+  // pairs).  It moves 1.01x the algorithmic DRAM bytes (vs 2x) but, with two
+  // 256-thread tile groups per SM (128 registers, ~200 KB smem), is bound by
+  // SM latency; it is the default only where the B200 A/B measured it faster
+  // (profiles/r02_fused_multipass.md): fp16 N = 2^14 (+0.6%), 2^16 (+3.9%)
+  // and fp32 N = 2^14 (+11%).  DSFFT_MP_FUSED=1 / 0 forces it on / off.
+  const bool fused_ok = !f16c && m % 2 == 0 && m >= 14 && m <= 18;
+  const bool fused_auto = precision == kFp16 ? (m == 14 || m == 16) : m == 14;
+  const int fused_env = env_or("DSFFT_MP_FUSED", -1);
+  mp->fused = fused_ok && (fused_env < 0 ? fused_auto : fused_env != 0);
   auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
   int P = 0;
   // two-word values (fp32, fp16 pairs) take s = 10 groups as 16-column tiles,

@@ -34,8 +34,12 @@ def test_random_cases(dsfft, cuda, orc, monkeypatch, case):
     in_place = bool(rng.randint(2))
     max_batch = max(1, (1 << 17) >> m)
     batch = int(rng.randint(1, max_batch + 1))
-    # half the large-N plans take the one-launch path (DSFFT_MP_FUSED, opt-in)
-    monkeypatch.setenv("DSFFT_MP_FUSED", str(int(rng.randint(2))))
+    # large-N path: the library default, forced two-launch, or forced fused
+    fused = int(rng.randint(3)) - 1
+    if fused < 0:
+        monkeypatch.delenv("DSFFT_MP_FUSED", raising=False)
+    else:
+        monkeypatch.setenv("DSFFT_MP_FUSED", str(fused))
     x = ref_inputs(orc, n, batch, seed=case, precision=precision)
     xw = x if precision == "fp64" else to_work(x, precision)
     plan = dsfft.make_plan(n, strategy, precision)

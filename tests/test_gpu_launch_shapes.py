@@ -41,6 +41,7 @@ def test_single_kernel_shapes(dsfft, cuda, orc, monkeypatch, n, precision, group
 @pytest.mark.parametrize("n,precision", [(1 << 14, "fp16"), (1 << 16, "fp32"),
                                          (1 << 19, "fp16")])
 def test_multipass_shapes(dsfft, cuda, orc, monkeypatch, n, precision, stages, groups):
+    monkeypatch.setenv("DSFFT_MP_FUSED", "0")  # the shapes are the two-launch kernel's
     monkeypatch.setenv("DSFFT_MP_STAGES", str(stages))
     monkeypatch.setenv("DSFFT_MP_GROUPS", str(groups))
     assert _run(dsfft, cuda, orc, n, precision, 5 if n <= 1 << 16 else 3, inverse=True) == 0

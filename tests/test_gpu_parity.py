@@ -197,8 +197,10 @@ LARGE = [2 ** m for m in range(13, 21)]
 @pytest.mark.parametrize("precision", ["fp32", "fp16"])
 @pytest.mark.parametrize("n", LARGE)
 @pytest.mark.parametrize("inverse", [False, True], ids=["fwd", "inv"])
-def test_multipass_bit_exact(dsfft, cuda, orc, n, precision, inverse):
-    """N = 2^13..2^20: 2-3 pass-group launches."""
+def test_multipass_bit_exact(dsfft, cuda, orc, monkeypatch, n, precision, inverse):
+    """N = 2^13..2^20: 2-3 pass-group launches (the two-launch path is forced
+    where the fused one is the default; test_fused_* cover that one)."""
+    monkeypatch.setenv("DSFFT_MP_FUSED", "0")
     chk = _checker()
     batch = 3 if n <= 1 << 16 else 2
     strategies = ALL_STRATEGIES if n <= 1 << 14 else ("dual", "lf")
@@ -230,6 +232,7 @@ def test_multipass_in_place(dsfft, cuda, orc, monkeypatch, n, chunk_mb):
     """in == out through 2- and 3-group splits with odd chunks: a chunk's last
     group overwrites only input its first group has already consumed."""
     monkeypatch.setenv("DSFFT_MP_CHUNK_MB", str(chunk_mb))
+    monkeypatch.setenv("DSFFT_MP_FUSED", "0")
     chk = _checker()
     x = ref_inputs(orc, n, 5, seed=n + 3, precision="fp16")
     plan = dsfft.make_plan(n, "dual", "fp16")
@@ -291,6 +294,7 @@ def test_multipass_odd_chunks(dsfft, cuda, orc, monkeypatch, n, precision, chunk
     """Chunked batches whose chunks hold an odd number of transforms: fp16
     pair-packed intermediates and pair partners across chunk boundaries."""
     monkeypatch.setenv("DSFFT_MP_CHUNK_MB", str(chunk_mb))
+    monkeypatch.setenv("DSFFT_MP_FUSED", "0")
     chk = _checker()
     x = ref_inputs(orc, n, batch, seed=n + batch, precision=precision)
     plan = dsfft.make_plan(n, "dual", precision)
@@ -457,6 +461,21 @@ def test_fused_multipass_bit_exact(dsfft, cuda, orc, monkeypatch, n, precision, 
         want = to_work((chk.inverse if inverse else chk.forward)(x, s, precision), precision)
         assert bit_mismatches(y, want) == 0, (n, s, precision, inverse)
         assert dsfft.last_launch_count() == 1
+
+
+@pytest.mark.parametrize("n,precision,launches", [
+    (1 << 14, "fp16", 1), (1 << 16, "fp16", 1), (1 << 18, "fp16", 2),
+    (1 << 14, "fp32", 1), (1 << 16, "fp32", 2), (1 << 18, "fp32", 2), (1 << 15, "fp16", 2)])
+def test_default_large_n_path(dsfft, cuda, orc, monkeypatch, n, precision, launches):
+    """With DSFFT_MP_FUSED unset the library takes the fused one-launch path
+    exactly where the B200 A/B measured it faster (multipass.cu), bit-exact."""
+    monkeypatch.delenv("DSFFT_MP_FUSED", raising=False)
+    chk = _checker()
+    x = ref_inputs(orc, n, 3, seed=n + 23, precision=precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = _device_run(dsfft, cuda, plan, to_work(x, precision), False)
+    assert bit_mismatches(y, to_work(chk.forward(x, "dual", precision), precision)) == 0
+    assert dsfft.last_launch_count() == launches
 
 
 @pytest.mark.parametrize("lag,slots,teams", [(1, None, None), (2, None, 3), (1, 4, 1)])

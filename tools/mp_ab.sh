@@ -1,6 +1,6 @@
 #!/bin/bash
-# A/B of the large-N paths on one GPU: fused one-launch (default for
-# N = 2^14/2^16/2^18) vs the two-launch path (DSFFT_MP_FUSED=0).
+# A/B of the large-N paths on one GPU: fused one-launch (DSFFT_MP_FUSED=1;
+# the default for fp16 2^14/2^16 and fp32 2^14) vs two launches (=0).
 # Prints one line per (N, precision, path): ms per step and roofline fraction.
 # usage: tools/mp_ab.sh [sizes...]   (run under gpurun)
 sizes=${@:-16384 65536 262144}
