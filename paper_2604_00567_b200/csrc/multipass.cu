@@ -54,6 +54,7 @@ struct MpParams {
   long long b_off;   // first transform of the chunk (tensor-map coordinate)
   long long tiles;   // nb * tiles_per_transform
   uint32_t scale;
+  int keep_l2;       // load tiles evict_normal (box rows narrower than a line)
 };
 
 // One pass group over all tiles of a chunk.  A CTA runs G = blockDim/T tile
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
   __syncthreads();
 
   uint64_t pol = 0;
-  if (leader) pol = ptx::policy_evict_first();
+  if (leader) pol = p.keep_l2 ? ptx::policy_evict_normal() : ptx::policy_evict_first();
   const int nb = int(p.nb);
   // TMA load of transform b of column block (q, rb) into ring slot `slot`
   // (fp16 pairs: transforms b and b+1 land in the two halves of the slot; a
@@ -291,6 +292,10 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
       vb == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64;
   const cuuint64_t N = cuuint64_t(1) << m;
   const cuuint32_t rows_box = cuuint32_t(std::min(1 << s, 256));
+  // 128-B promotion: a box row narrower than a line (16 fp16 columns = 64 B)
+  // still fetches the whole line; the neighbouring tile, loaded evict_normal
+  // (MpParams::keep_l2), then finds its half in L2
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r;
   if (P == 0) {  // {q (N/2^s), c (2^s), b}
@@ -299,14 +304,14 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
     cuuint32_t box[3] = {cuuint32_t(box_cols), rows_box, 1};
     r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (P + s == m) {  // last group: blocked intermediate {r_l, c, rb, b}
     cuuint64_t dims[4] = {32, cuuint64_t(1) << s, N >> (s + 5), cuuint64_t(batch)};
     cuuint64_t strides[3] = {32 * cuuint64_t(vb), (cuuint64_t(32) << s) * vb, N * vb};
     cuuint32_t box[4] = {cuuint32_t(box_cols), rows_box, 1, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {  // {r (2^P), q (N/2^(P+s)), c (2^s), b}
     cuuint64_t dims[4] = {cuuint64_t(1) << P, N >> (P + s), cuuint64_t(1) << s,
                           cuuint64_t(batch)};
@@ -314,7 +319,7 @@ int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
     cuuint32_t box[4] = {cuuint32_t(box_cols), 1, rows_box, 1};
     r = enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return int(r);
 }
@@ -563,6 +568,11 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       p.b_off = i == 0 ? (long long)b0 : 0;
       p.tiles = (((1LL << mp.m) >> g.s) / tile_cols(g.s)) * (long long)nb;
       p.scale = scale;
+      // first-group rows narrower than a 128-B line (fp16 s = 10: 16 x 4 B):
+      // with evict_first the line's other half was evicted before the next
+      // column block's tile read it -- 2x DRAM reads (ncu, 2^20 fp16); kept
+      // evict_normal it hits L2: 1.12 -> 1.00 ms per 1 GiB step
+      p.keep_l2 = env_or("DSFFT_MP_KEEP", i == 0 && tile_cols(g.s) * vb < 128);
       const bool first = i == 0, last = i == ng - 1;
       const int S1 = g.s - 5, cw = tile_cols(g.s);
       const bool ci = first && inverse, so = last && inverse, bo = i == ng - 2;
