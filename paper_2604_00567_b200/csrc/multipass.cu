@@ -504,10 +504,14 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const int vb = int(sample_bytes(mp.precision));
   const size_t tb = (size_t(1) << mp.m) * vb;
   // columns per tile: 16 for s = 10 (a 32 x 1024 tile of 8-byte values would
-  // not fit shared memory), or everywhere from s = 7 with DSFFT_MP_CW=16
-  auto tile_cols = [&](int s) {
-    return s == 10 || (env_or("DSFFT_MP_CW", 32) == 16 &&
-                       !(mp.precision == kFp16 && !mp.f16_pairs) && s >= 7)
+  // not fit shared memory), or from s = 7 in every group (DSFFT_MP_CW=16) or
+  // the groups of bit mask DSFFT_MP_CWMASK (tuning; no default gains > 1.5%,
+  // profiles/r02_fused_multipass.md)
+  const int cw_mask = env_or("DSFFT_MP_CW", 32) == 16 ? 7 : env_or("DSFFT_MP_CWMASK", 0);
+  auto tile_cols = [&](int i) {
+    const int s = mp.groups[i].s;
+    return s == 10 || (((cw_mask >> i) & 1) && !(mp.precision == kFp16 && !mp.f16_pairs) &&
+                       s >= 7)
                ? 16
                : 32;
   };
@@ -546,7 +550,7 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
     const bool packed = i > 0 && f16 && mp.f16_pairs;
     const int rc = make_in_map(&maps[i], base, mp.m, mp.groups[i].P, mp.groups[i].s,
                                packed ? 8 : vb, packed ? (nb + 1) / 2 : nb,
-                               tile_cols(mp.groups[i].s));
+                               tile_cols(i));
     if (rc != 0) {
       g_mp_err = "multipass: cuTensorMapEncodeTiled failed (CUresult " + std::to_string(rc) +
                  ", group " + std::to_string(i) + ", base " +
@@ -566,15 +570,15 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       p.P = g.P;
       p.nb = (long long)nb;
       p.b_off = i == 0 ? (long long)b0 : 0;
-      p.tiles = (((1LL << mp.m) >> g.s) / tile_cols(g.s)) * (long long)nb;
+      p.tiles = (((1LL << mp.m) >> g.s) / tile_cols(i)) * (long long)nb;
       p.scale = scale;
       // first-group rows narrower than a 128-B line (fp16 s = 10: 16 x 4 B):
       // with evict_first the line's other half was evicted before the next
       // column block's tile read it -- 2x DRAM reads (ncu, 2^20 fp16); kept
       // evict_normal it hits L2: 1.12 -> 1.00 ms per 1 GiB step
-      p.keep_l2 = env_or("DSFFT_MP_KEEP", i == 0 && tile_cols(g.s) * vb < 128);
+      p.keep_l2 = env_or("DSFFT_MP_KEEP", i == 0 && tile_cols(i) * vb < 128);
       const bool first = i == 0, last = i == ng - 1;
-      const int S1 = g.s - 5, cw = tile_cols(g.s);
+      const int S1 = g.s - 5, cw = tile_cols(i);
       const bool ci = first && inverse, so = last && inverse, bo = i == ng - 2;
       const int sm = mp.sm_count;
       const size_t oi = mp.smem_optin;
