@@ -427,9 +427,12 @@ MultipassPlan* multipass_create(const std::vector<TableEntry>& table, int m, int
   // 256-thread tile groups per SM (128 registers, ~200 KB smem), is bound by
   // SM latency; it is the default only where the B200 A/B measured it faster
   // (profiles/r02_fused_multipass.md): fp16 N = 2^14 (+0.6%), 2^16 (+3.9%)
-  // and fp32 N = 2^14 (+11%).  DSFFT_MP_FUSED=1 / 0 forces it on / off.
+  // and fp32 N = 2^14 (+11%), for the 6-FMA variants: the 10-op standard
+  // butterfly makes the SM-bound fused kernel slower (fp16 2^14: 35% vs 42% of
+  // the roofline).  DSFFT_MP_FUSED=1 / 0 forces it on / off.
   const bool fused_ok = !f16c && m % 2 == 0 && m >= 14 && m <= 18;
-  const bool fused_auto = precision == kFp16 ? (m == 14 || m == 16) : m == 14;
+  const bool fused_auto = strategy != kStandard &&
+                          (precision == kFp16 ? (m == 14 || m == 16) : m == 14);
   const int fused_env = env_or("DSFFT_MP_FUSED", -1);
   mp->fused = fused_ok && (fused_env < 0 ? fused_auto : fused_env != 0);
   auto rec = [&](long long k) { return pack_record(table[k], strategy, precision, f16c); };
@@ -518,7 +521,10 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const bool f16 = mp.precision == kFp16;
   const bool std_ = mp.strategy == kStandard;
   const int ng = int(mp.groups.size());
-  if (mp.fused) return fused_execute(mp, inverse, in, out, batch, scale, stream, launches);
+  if (mp.fused) {
+    const int rc = fused_execute(mp, inverse, in, out, batch, scale, stream, launches);
+    if (rc != kFusedUnfit) return rc;
+  }
   // per-call, stream-ordered intermediates (plans may run on several streams)
   const size_t chunk = std::min(mp.chunk_transforms, batch);
   uint8_t* scratch[2] = {nullptr, nullptr};

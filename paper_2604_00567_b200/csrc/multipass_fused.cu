@@ -270,12 +270,11 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
   const bool std_ = mp.strategy == kStandard;
   const int s = mp.m / 2, S1 = s - 5;
   const long long units = f16 ? (long long)(batch + 1) / 2 : (long long)batch;
-  const FusedShape f = f16 ? fused_shape_a<ArithF16P>(S1, mp.m, mp.sm_count, mp.smem_optin, units)
-                           : fused_shape_a<ArithF32>(S1, mp.m, mp.sm_count, mp.smem_optin, units);
-  if (f.K == 0) {
-    set_mp_error("multipass: fused kernel does not fit");
-    return 1;
-  }
+  // DSFFT_FUSED_SMS caps the SMs a team may span (tests the unfit fallback)
+  const int sms = std::max(1, std::min(mp.sm_count, env_or("DSFFT_FUSED_SMS", mp.sm_count)));
+  const FusedShape f = f16 ? fused_shape_a<ArithF16P>(S1, mp.m, sms, mp.smem_optin, units)
+                           : fused_shape_a<ArithF32>(S1, mp.m, sms, mp.smem_optin, units);
+  if (f.K == 0) return kFusedUnfit;
   const size_t unit_bytes = (size_t(1) << mp.m) * 8;  // pair-packed fp16 / one fp32 transform
   const size_t slots = size_t(f.teams) * f.R;
   const size_t flag_bytes = 2 * slots * sizeof(uint32_t);
@@ -326,6 +325,10 @@ int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, si
   else
     e = std_ ? fused_launch_a<ArithF32, true>(S1, in_map, mid_map, p, f, inverse, stream)
              : fused_launch_a<ArithF32, false>(S1, in_map, mid_map, p, f, inverse, stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();  // not sticky: clear it for the two-launch path
+    return kFusedUnfit;
+  }
   if (e != cudaSuccess) {
     set_mp_error(std::string("mp_fused_kernel launch: ") + cudaGetErrorString(e));
     return 1;

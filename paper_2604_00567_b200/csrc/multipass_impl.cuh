@@ -279,7 +279,11 @@ int env_or(const char* name, int dflt);
 // TMA map over `batch` transforms at `base` for pass group [P, P+s) (see multipass.cu)
 int make_in_map(CUtensorMap* map, const void* base, int m, int P, int s, int vb,
                 long long batch, int box_cols = 32);
-// one-launch execution of an eligible plan (multipass_fused.cu)
+// one-launch execution of an eligible plan (multipass_fused.cu); returns
+// kFusedUnfit, with nothing launched, when the device cannot hold one team
+// co-resident (few SMs, small shared memory): the caller runs the same pass
+// groups as two launches
+constexpr int kFusedUnfit = 2;
 int fused_execute(MultipassPlan& mp, bool inverse, const void* in, void* out, size_t batch,
                   uint32_t scale, cudaStream_t stream, uint64_t* launches);
 

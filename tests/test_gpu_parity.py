@@ -463,19 +463,36 @@ def test_fused_multipass_bit_exact(dsfft, cuda, orc, monkeypatch, n, precision, 
         assert dsfft.last_launch_count() == 1
 
 
-@pytest.mark.parametrize("n,precision,launches", [
-    (1 << 14, "fp16", 1), (1 << 16, "fp16", 1), (1 << 18, "fp16", 2),
-    (1 << 14, "fp32", 1), (1 << 16, "fp32", 2), (1 << 18, "fp32", 2), (1 << 15, "fp16", 2)])
-def test_default_large_n_path(dsfft, cuda, orc, monkeypatch, n, precision, launches):
+@pytest.mark.parametrize("n,precision,strategy,launches", [
+    (1 << 14, "fp16", "dual", 1), (1 << 16, "fp16", "dual", 1), (1 << 18, "fp16", "dual", 2),
+    (1 << 14, "fp32", "lf", 1), (1 << 16, "fp32", "dual", 2), (1 << 18, "fp32", "dual", 2),
+    (1 << 15, "fp16", "dual", 2), (1 << 14, "fp16", "standard", 2),
+    (1 << 16, "fp16", "cosine", 1)])
+def test_default_large_n_path(dsfft, cuda, orc, monkeypatch, n, precision, strategy, launches):
     """With DSFFT_MP_FUSED unset the library takes the fused one-launch path
     exactly where the B200 A/B measured it faster (multipass.cu), bit-exact."""
     monkeypatch.delenv("DSFFT_MP_FUSED", raising=False)
     chk = _checker()
     x = ref_inputs(orc, n, 3, seed=n + 23, precision=precision)
-    plan = dsfft.make_plan(n, "dual", precision)
+    plan = dsfft.make_plan(n, strategy, precision)
     y = _device_run(dsfft, cuda, plan, to_work(x, precision), False)
-    assert bit_mismatches(y, to_work(chk.forward(x, "dual", precision), precision)) == 0
+    assert bit_mismatches(y, to_work(chk.forward(x, strategy, precision), precision)) == 0
     assert dsfft.last_launch_count() == launches
+
+
+@pytest.mark.parametrize("n,precision", [(1 << 16, "fp16"), (1 << 14, "fp32")])
+def test_fused_unfit_falls_back_to_two_launches(dsfft, cuda, orc, monkeypatch, n, precision):
+    """A device that cannot hold one team co-resident (here: teams capped to
+    fewer SMs than a team's K members) runs the same pass groups as two
+    launches -- on the GPU, bit-exact -- instead of failing."""
+    monkeypatch.delenv("DSFFT_MP_FUSED", raising=False)
+    monkeypatch.setenv("DSFFT_FUSED_SMS", "2")
+    chk = _checker()
+    x = ref_inputs(orc, n, 3, seed=n + 29, precision=precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    y = _device_run(dsfft, cuda, plan, to_work(x, precision), True)
+    assert bit_mismatches(y, to_work(chk.inverse(x, "dual", precision), precision)) == 0
+    assert dsfft.last_launch_count() == 2
 
 
 @pytest.mark.parametrize("lag,slots,teams", [(1, None, None), (2, None, 3), (1, 4, 1)])

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 out=gpurun_out/sweep.jsonl
 : > "$out"
 NS=${NS:-"64 128 256 512 1024 2048 4096 8192"}
-LARGE=${LARGE:-"16384 65536 262144 1048576 16777216"}
+LARGE=${LARGE:-"16384 32768 65536 131072 262144 524288 1048576 16777216"}
 for n in $NS; do
   for p in fp16 fp32; do
     sb=$([ "$p" = fp16 ] && echo 4 || echo 8)
