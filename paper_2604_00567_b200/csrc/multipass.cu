@@ -340,8 +340,9 @@ cudaError_t mp_launch_t(const CUtensorMap& map, const MpParams& p, bool first, b
   // short -- two 1-deep groups beat one 2-deep group by 0-3% (B200 sweep).
   const char* es = std::getenv("DSFFT_MP_STAGES");
   const char* eg = std::getenv("DSFFT_MP_GROUPS");
+  // 8-column tiles: one 2-deep group measured ahead of two 1-deep ones
   int stages = es && *es ? std::max(1, std::atoi(es)) : 2;
-  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : 512 / Lay::T;
+  int groups = eg && *eg ? std::max(1, std::atoi(eg)) : CW == 8 ? 1 : 512 / Lay::T;
   groups = std::min(groups, std::max(1, 512 / Lay::T));
   while (stages > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --stages;
   while (groups > 1 && Lay::smem_bytes(first, stages, groups) > smem_optin) --groups;
@@ -383,6 +384,7 @@ cudaError_t mp_launch_a(int S1, int cw, const CUtensorMap& map, const MpParams& 
 #define DSFFT_MP_GO(S, C) \
   mp_launch_t<S, A, STD, C>(map, p, first, conj_in, scale_out, last, bout, sm_count, optin, st)
   if constexpr (A::kWords == 2) {
+    if (cw == 8 && S1 == 5) return DSFFT_MP_GO(5, 8);  // s = 10: 8 x 1024 tiles (64 KB)
     if (cw == 16) {
       switch (S1) {
         case 2: return DSFFT_MP_GO(2, 16);
@@ -511,9 +513,15 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   // the groups of bit mask DSFFT_MP_CWMASK (tuning; no default gains > 1.5%,
   // profiles/r02_fused_multipass.md)
   const int cw_mask = env_or("DSFFT_MP_CW", 32) == 16 ? 7 : env_or("DSFFT_MP_CWMASK", 0);
+  // s = 10 groups in the bit mask DSFFT_MP_CW10MASK take 8-column x 1024-row
+  // tiles (64 KB, one 2-deep 256-thread group): default for the fp32 first
+  // group, +8% at 2^19 and 2^20; fp16 (32-byte input rows, 32-byte unpacked
+  // output runs) and later groups measured slower (profiles/r02_fused_multipass.md)
+  const int cw10_mask = env_or("DSFFT_MP_CW10MASK", mp.precision == kFp32 ? 1 : 0);
   auto tile_cols = [&](int i) {
     const int s = mp.groups[i].s;
-    return s == 10 || (((cw_mask >> i) & 1) && !(mp.precision == kFp16 && !mp.f16_pairs) &&
+    if (s == 10) return (cw10_mask >> i) & 1 ? 8 : 16;
+    return (((cw_mask >> i) & 1) && !(mp.precision == kFp16 && !mp.f16_pairs) &&
                        s >= 7)
                ? 16
                : 32;

@@ -34,7 +34,15 @@ template <int S1, class A, int CW = 32>
 struct MpLayout {
   static constexpr int s = 5 + S1, L = 1 << s, T = CW << S1;
   static constexpr int VB = A::kWords * 4;
-  static constexpr int kBufBytes = CW * (L + 1) * VB;  // padded exchange >= TMA tile
+  // exchange layout [col][local pos]: column stride L + 1 values; 8-column
+  // tiles (four row phases per warp) pad one value per 32 and use a column
+  // stride = 4 mod 16 so both exchange walks stay at two wavefronts
+  static constexpr bool kPadX = CW == 8;
+  static constexpr int kColStride = kPadX ? ((L + L / 32 + 11) / 16) * 16 + 4 : L + 1;
+  __host__ __device__ static constexpr int xpos(int c, int pos) {
+    return c * kColStride + (kPadX ? pos + (pos >> 5) : pos);
+  }
+  static constexpr int kBufBytes = CW * kColStride * VB;  // padded exchange >= TMA tile
   static constexpr int kTileBytes = CW * L * VB;
   // twiddle area rounded to 128 B: TMA tensor destinations are 128-B aligned.
   // Later groups keep their column block's whole twiddle slab in smem (stage 1
@@ -75,7 +83,6 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   constexpr int NSUB = 32 / CW;        // row phases per warp
   const int sub = warp * NSUB + (NSUB == 1 ? 0 : lane / CW);
   const int col = lane % CW, col32 = col_off + col;
-  constexpr int STRIDE = L + 1;  // padded exchange column (values)
   constexpr int RB = A::kRecBytes;
   constexpr int PAIR = A::kPair;
   constexpr int EB = A::kSampleBytes;  // bytes of one complex in memory
@@ -130,7 +137,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
   group_sync();  // every stage-1 read of the TMA tile is done
 #pragma unroll
   for (int cc = 0; cc < 32; ++cc) {
-    const uint32_t a = buf + (col * STRIDE + sub * 32 + cc) * VB;
+    const uint32_t a = buf + Lay::xpos(col, sub * 32 + cc) * VB;
     if constexpr (A::kWords == 1) ptx::sts32(a, re[cc]); else ptx::sts64(a, re[cc], im[cc]);
   }
   group_sync();
@@ -142,7 +149,7 @@ __device__ __forceinline__ void mp_tile(uint32_t buf, uint32_t tw_base, const ui
     const int rl_ = FIRST ? lane : sub + (j << S1);
 #pragma unroll
     for (int cc = 0; cc < (1 << S1); ++cc) {
-      const uint32_t a = buf + (col2 * STRIDE + rl_ + 32 * cc) * VB;
+      const uint32_t a = buf + Lay::xpos(col2, rl_ + 32 * cc) * VB;
       const int v = (j << S1) + cc;
       if constexpr (A::kWords == 1) re[v] = ptx::lds32(a); else ptx::lds64(a, re[v], im[v]);
     }

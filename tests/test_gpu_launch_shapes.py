@@ -58,3 +58,12 @@ def test_fused_shapes(dsfft, cuda, orc, monkeypatch, n, precision, lag, slots, t
     if teams:
         monkeypatch.setenv("DSFFT_FUSED_TEAMS", str(teams))
     assert _run(dsfft, cuda, orc, n, precision, 37 if n == 1 << 14 else 13) == 0
+
+
+@pytest.mark.parametrize("mask", [1, 2, 3])
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_s10_tile_widths(dsfft, cuda, orc, monkeypatch, precision, mask):
+    """s = 10 pass groups on 8- or 16-column tiles (DSFFT_MP_CW10MASK; the
+    default is 8 for the fp32 first group only), N = 2^20, inverse."""
+    monkeypatch.setenv("DSFFT_MP_CW10MASK", str(mask))
+    assert _run(dsfft, cuda, orc, 1 << 20, precision, 3, inverse=True) == 0
