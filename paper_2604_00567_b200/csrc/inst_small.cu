@@ -58,6 +58,13 @@ using CfgC = CfgW;
 #error "single-kernel path covers N <= 8192"
 #endif
 
+#ifdef DSFFT_OV_E  // schedule experiments (tools/sched_variants.py)
+using CfgWX = Sched<DSFFT_M, DSFFT_OV_E, DSFFT_OV_W, DSFFT_OV_S0, DSFFT_OV_S1, DSFFT_OV_S2,
+                    DSFFT_OV_S3>;
+#else
+using CfgWX = CfgW;
+#endif
+
 // fp32 at N = 256 / 512: 16 values per thread (E=16, ~80 registers) and more
 // resident warps beat E=32 (B200 sweep at >= 4 GiB per step: +2% / +4%)
 #if DSFFT_M == 8
@@ -65,14 +72,14 @@ using CfgF = Sched<8, 4, 1, 4, 4>;
 #elif DSFFT_M == 9
 using CfgF = Sched<9, 4, 1, 4, 4, 1>;
 #else
-using CfgF = CfgW;
+using CfgF = CfgWX;
 #endif
 #define DSFFT_CAT2(a, b) a##b
 #define DSFFT_CAT(a, b) DSFFT_CAT2(a, b)
 SmallEntry DSFFT_CAT(small_entry_m, DSFFT_M)() {
   SmallEntry e{};
   e.v[kVarF32] = make_variant<CfgF, ArithF32>();
-  e.v[kVarF16P] = make_variant<CfgW, ArithF16P>();
+  e.v[kVarF16P] = make_variant<CfgWX, ArithF16P>();
   e.v[kVarF16C] = make_variant<CfgC, ArithF16C>();
   // Defaults from B200 sweeps (profiles/README.md, "launch shapes"):
   // with 8-byte records, fp16 transform pairs win from N = 128 (95-97% of HBM
