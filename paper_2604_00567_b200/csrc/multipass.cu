@@ -515,7 +515,7 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
   const int cw_mask = env_or("DSFFT_MP_CW", 32) == 16 ? 7 : env_or("DSFFT_MP_CWMASK", 0);
   // s = 10 groups in the bit mask DSFFT_MP_CW10MASK take 8-column x 1024-row
   // tiles (64 KB, one 2-deep 256-thread group): default for the fp32 first
-  // group, +8% at 2^19 and 2^20; fp16 (32-byte input rows, 32-byte unpacked
+  // group, +11% at 2^19 and 2^20; fp16 (32-byte input rows, 32-byte unpacked
   // output runs) and later groups measured slower (profiles/r02_fused_multipass.md)
   const int cw10_mask = env_or("DSFFT_MP_CW10MASK", mp.precision == kFp32 ? 1 : 0);
   auto tile_cols = [&](int i) {

@@ -36,9 +36,10 @@ struct MpLayout {
   static constexpr int VB = A::kWords * 4;
   // exchange layout [col][local pos]: column stride L + 1 values; 8-column
   // tiles (four row phases per warp) pad one value per 32 and use a column
-  // stride = 4 mod 16 so both exchange walks stay at two wavefronts
+  // stride = 2 mod 16 values: a 64-bit access is served per half-warp (8
+  // columns x 2 row phases), whose 16 values then hit 16 distinct bank pairs
   static constexpr bool kPadX = CW == 8;
-  static constexpr int kColStride = kPadX ? ((L + L / 32 + 11) / 16) * 16 + 4 : L + 1;
+  static constexpr int kColStride = kPadX ? ((L + L / 32 + 13) / 16) * 16 + 2 : L + 1;
   __host__ __device__ static constexpr int xpos(int c, int pos) {
     return c * kColStride + (kPadX ? pos + (pos >> 5) : pos);
   }
