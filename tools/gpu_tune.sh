@@ -13,7 +13,18 @@
 #     DSFFT_MP_STAGES     ring depth;  DSFFT_MP_GROUPS  tile groups per CTA
 #     DSFFT_MP_CHUNK_MB   batch chunk per launch sequence
 #     DSFFT_MP_F16_LAYOUT 1 = transform pairs, 2 = one complex per register
-#     DSFFT_MP_SPLIT      pass-group sizes, e.g. "9,7" (each 6..9, summing to log2 N)
+#     DSFFT_MP_SPLIT      pass-group sizes, e.g. "9,7" (each 6..10, summing to log2 N)
+#     DSFFT_MP_FUSED      1 / 0: force the one-launch (L2-resident) path on / off
+#                         (N = 2^14, 2^16, 2^18; default on for fp16 2^14 / 2^16
+#                         and fp32 2^14, 6-FMA variants)
+#     DSFFT_FUSED_LAG / DSFFT_FUSED_SLOTS / DSFFT_FUSED_TEAMS / DSFFT_FUSED_GROUPS /
+#     DSFFT_FUSED_SMS     one-launch lag (units), ring slots, teams, tile groups, SM cap
+#     DSFFT_MP_CW=16      16-column tiles in every group from s = 7;
+#     DSFFT_MP_CWMASK     ... in the groups of this bit mask only
+#     DSFFT_MP_CW10MASK   s = 10 groups of this bit mask on 8-column tiles
+#                         (default: the fp32 first group)
+#     DSFFT_MP_KEEP       1 / 0: load tiles evict_normal / evict_first (default:
+#                         evict_normal only for first-group rows < 128 B)
 #   host pipeline
 #     DSFFT_HOST_CHUNK_MB chunk of dsfft_execute_host's H2D/kernel/D2H pipeline
 #   A/B builds
