@@ -1,13 +1,14 @@
 // multipass.cu -- batched forward/inverse for N = 2^14 .. 2^24 (and 2^13 on request).
 //
 // The m = log2 N passes are split into 2-3 consecutive pass groups
-// [P, P+s), s in 6..9, each one launch of mp_kernel (SURVEY.md A.1 item 3
+// [P, P+s), s in 6..10, each one launch of mp_kernel (SURVEY.md A.1 item 3
 // regrouping, bit-exact).  A pass group works on independent groups
 // g = q*2^P + r: group g gathers x[g + c*N/2^s] (c < 2^s), runs s radix-2
 // passes whose butterflies use the reference's table entries
 // (r + 2^P*rl') * N/2^(P+pl'+1), and scatters to q*2^(P+s) + r + 2^P*c'.
 //
-// CTA tile = 32 consecutive groups ("columns") x 2^s rows:
+// CTA tile = CW consecutive groups ("columns") x 2^s rows (CW = 32; 16 or 8
+// for s = 10, whose 32-column tiles would not fit shared memory):
 //   * first group (P = 0): columns are 32 consecutive q; each column's
 //     outputs are 2^s contiguous samples;
 //   * later groups (P >= 6): columns are 32 consecutive r at fixed q; every
@@ -23,7 +24,8 @@
 // Between groups the intermediate is blocked for the last group (each of its
 // tiles one contiguous block) and, for fp16, pair-packed (8-byte values of
 // transforms b, b+1).  The batch runs in chunks of up to 1 GiB
-// (DSFFT_MP_CHUNK_MB); L2-sized chunks were measured slower.
+// (DSFFT_MP_CHUNK_MB); L2-sized chunks were measured slower.  N = 2^14 /
+// 2^16 (fp16) and 2^14 (fp32) take the one-launch path of multipass_fused.cu.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -235,7 +237,7 @@ EncodeFn encode_fn() {
 
 std::vector<int> split_passes(int m, int max_s, bool fp32) {
   // DSFFT_MP_SPLIT="a,b[,c]" overrides (tuning; ignored unless every group is
-  // 6..9 passes and they sum to m)
+  // 6..max_s passes and they sum to m)
   if (const char* env = std::getenv("DSFFT_MP_SPLIT")) {
     std::vector<int> v;
     int sum = 0;
