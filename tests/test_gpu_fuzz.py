@@ -55,12 +55,14 @@ def test_random_cases(dsfft, cuda, orc, monkeypatch, case):
                                                                    inverse, batch)
 
 
-@pytest.mark.parametrize("n,precision", [(1024, "fp16"), (1 << 15, "fp16"), (512, "fp32")])
+@pytest.mark.parametrize("n,precision", [(1024, "fp16"), (1 << 15, "fp16"), (512, "fp32"),
+                                         (1 << 16, "fp16"), (1 << 14, "fp32"), (1 << 20, "fp32")])
 def test_cuda_graph_capture(dsfft, cuda, orc, n, precision):
     """dsfft_execute is stream-ordered and capturable: a captured graph replays
-    the same bits (multipass scratch becomes graph memory nodes)."""
+    the same bits (multipass scratch becomes graph memory nodes; the fused
+    one-launch path at 2^16 fp16 / 2^14 fp32 is a cooperative kernel node)."""
     torch = cuda
-    batch = 8
+    batch = 8 if n < 1 << 20 else 2
     x = ref_inputs(orc, n, batch, seed=3, precision=precision)
     xt = torch.from_numpy(to_work(x, precision)).cuda()
     yt = torch.empty_like(xt)
