@@ -98,6 +98,23 @@ def test_host_buffer_paths(dsfft, cuda, orc):
     assert back.tobytes() == chk.inverse(got, "dual", "fp32").tobytes()
 
 
+@pytest.mark.parametrize("n,precision", [(1 << 16, "fp16"), (1 << 14, "fp32"), (1 << 20, "fp32")])
+def test_host_pipeline_large_n(dsfft, cuda, orc, monkeypatch, n, precision):
+    """dsfft_execute_host over small chunks: three pipe streams run chunk
+    kernels concurrently -- for 2^16 fp16 / 2^14 fp32 these are the fused
+    cooperative kernels -- and the result equals the reference's bits."""
+    sb = 4 if precision == "fp16" else 8
+    monkeypatch.setenv("DSFFT_HOST_CHUNK_MB", str(max(1, (4 * n * sb) >> 20)))
+    batch = 37 if n < 1 << 20 else 5
+    chk = _checker()
+    x = ref_inputs(orc, n, batch, seed=n + 41, precision=precision)
+    plan = dsfft.make_plan(n, "dual", precision)
+    xw = to_work(x, precision)
+    out = np.empty_like(xw)
+    dsfft.execute_host(plan, 0, xw, out, batch)
+    assert bit_mismatches(out, to_work(chk.forward(x, "dual", precision), precision)) == 0
+
+
 def test_nonfinite_propagates(dsfft, cuda, orc):
     """test_fft.cpp:252-262: NaN input propagates; cosine fp16 is non-finite."""
     n = 8
