@@ -57,6 +57,7 @@ struct MpParams {
   long long tiles;   // nb * tiles_per_transform
   uint32_t scale;
   int keep_l2;       // load tiles evict_normal (box rows narrower than a line)
+  int prefetch;      // L2-prefetch the tile this many ring turns ahead (0: off)
 };
 
 // One pass group over all tiles of a chunk.  A CTA runs G = blockDim/T tile
@@ -129,6 +130,20 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
           ptx::tma_load_4d(d, &in_map, rb * 32 + hf * CW, int(q), r0, bb, &bars[slot], pol);
       }
   };
+  auto prefetch_load = [&](long long q, int rb, int hf, int b) {
+#pragma unroll
+    for (int h = 0; h < (PIN ? 1 : PAIR); ++h)
+#pragma unroll
+      for (int r0 = 0; r0 < L; r0 += ROWS_BOX) {
+        const int bb = PIN ? b / 2 : int(b + h + p.b_off);
+        if constexpr (FIRST)
+          ptx::tma_prefetch_3d(&in_map, int(q * CW), r0, bb);
+        else if constexpr (LAST)
+          ptx::tma_prefetch_4d(&in_map, hf * CW, r0, rb, bb);
+        else
+          ptx::tma_prefetch_4d(&in_map, rb * 32 + hf * CW, int(q), r0, bb);
+      }
+  };
   auto tile = [&](long long q, int rb, int hf, int b, bool second, uint32_t buf,
                   auto&& release) {
     mp_tile<S1, A, STANDARD, FIRST, CONJ_IN, SCALE_OUT, LAST, BOUT, CW>(
@@ -152,6 +167,12 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
       const long long idx = first_idx + (long long)G * i;
       const long long pr = idx / nblk;
       issue_load(idx - pr * nblk, 0, 0, int(pr * PAIR), i % S);
+      const int ip = i + p.prefetch * S;
+      if (p.prefetch && ip < k) {
+        const long long idp = first_idx + (long long)G * ip;
+        const long long prp = idp / nblk;
+        prefetch_load(idp - prp * nblk, 0, 0, int(prp * PAIR));
+      }
     };
     if (leader)
       for (int i = 0; i < S && i < k; ++i) load_tile(i);
@@ -196,16 +217,20 @@ __global__ void __launch_bounds__(512) __maxnreg__(A::kWords == 1 ? 80 : 128)
       const int k = units > g ? (units - g + G - 1) / G : 0;  // this group's tiles
       auto item_b = [&](int i) { return int(PAIR * ((w0 + g + (long long)G * i) / HPB)); };
       auto item_hf = [&](int i) { return int((w0 + g + (long long)G * i) % HPB); };
+      auto load_item = [&](int i) {
+        issue_load(q, rb, item_hf(i), item_b(i), int((it + i) % S));
+        const int ip = i + p.prefetch * S;
+        if (p.prefetch && ip < k) prefetch_load(q, rb, item_hf(ip), item_b(ip));
+      };
       if (leader)
-        for (int i = 0; i < S && i < k; ++i)
-          issue_load(q, rb, item_hf(i), item_b(i), int((it + i) % S));
+        for (int i = 0; i < S && i < k; ++i) load_item(i);
       for (int i = 0; i < k; ++i) {
         const int b = item_b(i);
         const int slot = int((it + i) % S);
         ptx::mbar_wait(&bars[slot], uint32_t(((it + i) / S) & 1));
         tile(q, rb, item_hf(i), b, PAIR == 2 && b + 1 < nb,
              ptx::smem_u32(bufs + size_t(slot) * Lay::kBufBytes), [&] {
-               if (leader && i + S < k) issue_load(q, rb, item_hf(i + S), item_b(i + S), slot);
+               if (leader && i + S < k) load_item(i + S);
              });
       }
       it += k;
@@ -593,6 +618,14 @@ int multipass_execute(MultipassPlan& mp, bool inverse, const void* in, void* out
       // column block's tile read it -- 2x DRAM reads (ncu, 2^20 fp16); kept
       // evict_normal it hits L2: 1.12 -> 1.00 ms per 1 GiB step
       p.keep_l2 = env_or("DSFFT_MP_KEEP", i == 0 && tile_cols(i) * vb < 128);
+      // later groups of s = 9 (and s = 10 for fp16 pairs) run 128 KB tiles
+      // 1-deep: an L2 prefetch of the next tile, issued with this one's load,
+      // hides part of its latency (+3-4% at 2^17 - 2^20).  First groups (user
+      // input; 8-column / evict_normal loads) and fp32 s = 10 last groups
+      // measured slower with it (profiles/r02_fused_multipass.md)
+      const bool pf = i > 0 && (g.s == 9 || (g.s == 10 && f16 && mp.f16_pairs));
+      p.prefetch = env_or("DSFFT_MP_PREFETCH",
+                          (env_or("DSFFT_MP_PFMASK", pf ? 1 << i : 0) >> i) & 1);
       const bool first = i == 0, last = i == ng - 1;
       const int S1 = g.s - 5, cw = tile_cols(i);
       const bool ci = first && inverse, so = last && inverse, bo = i == ng - 2;

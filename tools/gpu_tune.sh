@@ -25,6 +25,9 @@
 #                         (default: the fp32 first group)
 #     DSFFT_MP_KEEP       1 / 0: load tiles evict_normal / evict_first (default:
 #                         evict_normal only for first-group rows < 128 B)
+#     DSFFT_MP_PREFETCH   1 / 0: L2-prefetch the next tile in every group / none;
+#     DSFFT_MP_PFMASK     ... in the groups of this bit mask (default: later
+#                         groups with s = 9, or s = 10 for fp16 pairs)
 #   host pipeline
 #     DSFFT_HOST_CHUNK_MB chunk of dsfft_execute_host's H2D/kernel/D2H pipeline
 #   A/B builds
