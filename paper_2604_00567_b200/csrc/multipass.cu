@@ -292,9 +292,10 @@ std::vector<int> split_passes(int m, int max_s, bool fp32) {
     // 8-byte values: the larger group last (the first group reads the user's
     // rows, the last the blocked intermediate), except where the B200 sweep
     // (profiles/r02_fused_multipass.md, "pass-group splits") measured the
-    // other way for fp32: m = 18 and 19 as 10 + 8 / 10 + 9, the s = 10 first
-    // group on 8-column tiles (2^18: +7% over 8 + 10, +18% over 9 + 9)
-    const int a = fp32 && (m == 18 || m == 19) ? 10 : m / 2;
+    // other way: m = 19 as 10 + 9 (fp16 +2% since its s = 10 first group
+    // loads evict_normal; fp32 with that group on 8-column tiles) and fp32
+    // m = 18 as 10 + 8 (+7% over 8 + 10, +18% over 9 + 9)
+    const int a = m == 19 || (fp32 && m == 18) ? 10 : m / 2;
     return {a, m - a};
   }
   const int a = (m + 2) / 3, b = (m - a + 1) / 2;
